@@ -1,0 +1,151 @@
+/*
+ * adamas_b200.h — C ABI of the B200-native Adamas decode hot path.
+ *
+ * This is the drop-in boundary for the reference's operator layer
+ * (/root/reference/proj, namespace adamas). The reference binds its hot path
+ * per (query, key) pair through the function table kernels::Kernels
+ * (include/adamas/kernels.hpp:16-33) called S times per decode; a GPU cannot
+ * plug in at that granularity, so this ABI replaces the operator level instead,
+ * batched over heads and tokens with one opaque device cache per layer.
+ * Every entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain C types only. Device pointers are raw CUDA device addresses; the
+ *     `stream` argument is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - head_dim is 128 and bits is 2 (the north-star scope); anything else is
+ *     rejected with ADAMAS_ERR_CONFIG, never silently mis-computed.
+ *   - K/V/q element type: ADAMAS_F32 or ADAMAS_BF16 (fixed per cache).
+ *   - Layouts: q [n_q_heads][128]; new keys/values [n_tokens][n_kv_heads][128];
+ *     attention output float32 [n_q_heads][128]; indices int32
+ *     [n_q_heads][budget] ascending (min(budget, seq_len) valid per head).
+ *   - GQA: q-head h reads kv-head h / (n_q_heads / n_kv_heads); every q-head
+ *     is encoded, scanned, selected and attended independently, exactly like
+ *     independent reference heads.
+ *   - Return codes mirror the reference's exception classes:
+ *       ADAMAS_ERR_CONFIG  <-> adamas::ConfigError (common.hpp:19-22)
+ *       ADAMAS_ERR_RUNTIME <-> std::runtime_error / CUDA failures
+ *     adamas_last_error() returns the thread-local message of the last failure.
+ *   - Per-vector preconditions the reference checks with exceptions (zero or
+ *     non-finite vector, quantizer.cpp:46-47) are detected on the device and
+ *     latched into a sticky status word: adamas_cache_status().
+ */
+#ifndef ADAMAS_B200_H
+#define ADAMAS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADAMAS_OK 0
+#define ADAMAS_ERR_CONFIG 1
+#define ADAMAS_ERR_RUNTIME 2
+
+#define ADAMAS_F32 0
+#define ADAMAS_BF16 1
+
+/* Sticky device status bits. */
+#define ADAMAS_STATUS_DEGENERATE 1 /* a zero / non-finite vector was encoded */
+
+typedef struct adamas_cache adamas_cache;
+
+/* Version string of the library build. */
+const char* adamas_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* adamas_last_error(void);
+
+/* ---------------------------------------------------------------- cache
+ * Replaces KvCache(head_dim, bits) (kv_cache.cpp:32-41), batched over the
+ * layer's kv-heads, with device storage for `capacity` tokens per head:
+ * K, V in kv_dtype and 32 B of codes per token per head. Rejects
+ * head_dim != 128, bits != 2, n_kv_heads < 1 or capacity < 1. */
+int adamas_cache_create(adamas_cache** out, int n_kv_heads, int head_dim, int bits,
+                        int64_t capacity, int kv_dtype);
+int adamas_cache_destroy(adamas_cache* cache);
+/* KvCache::seq_len (kv_cache.hpp:23). */
+int adamas_cache_seq_len(const adamas_cache* cache, int64_t* out);
+/* Rewinds the sequence length (tokens past it are forgotten). 0 <= seq_len <= current. */
+int adamas_cache_truncate(adamas_cache* cache, int64_t seq_len);
+/* Device addresses of the cache arrays (for callers fusing their own kernels). */
+int adamas_cache_buffers(const adamas_cache* cache, void** keys, void** values, void** codes);
+/* Reads and clears the sticky device status word (synchronizes the stream). */
+int adamas_cache_status(adamas_cache* cache, void* stream, int* status);
+
+/* Fused encode + append. Replaces, for every token and kv-head,
+ * KvCache::update(k, v, pack(encode(k))) (kv_cache.cpp:62-71 with
+ * sweep.cpp:32-36, :44-47 — the build_cache loop, sweep.cpp:38-50).
+ * keys/values: device [n_tokens][n_kv_heads][128]. Used for single-token
+ * decode appends and for bulk prefill alike. */
+int adamas_cache_append(adamas_cache* cache, const void* keys, const void* values, int64_t n_tokens,
+                        void* stream);
+
+/* Append with caller-supplied codes in the REFERENCE word layout
+ * (PackedCodes.words, quantizer.hpp:44-50): KvCache::update(k, v, code).
+ * codes_ref: device uint16 [n_tokens][n_kv_heads][16]. */
+int adamas_cache_append_coded(adamas_cache* cache, const void* keys, const void* values,
+                              const uint16_t* codes_ref, int64_t n_tokens, void* stream);
+
+/* Copies codes of tokens [start, start+n) of every kv-head out in the reference
+ * word layout (KvCache::code_words, kv_cache.hpp:35-37) into device uint16
+ * [n_kv_heads][n][16]. */
+int adamas_cache_codes_ref(const adamas_cache* cache, int64_t start, int64_t n, uint16_t* out_ref,
+                           void* stream);
+
+/* ---------------------------------------------------------------- operators */
+
+/* pack(encode(q)) per q-head (sweep.cpp:92-94): q device [n_q_heads][128] in the
+ * cache's dtype -> device uint16 [n_q_heads][16] reference-layout words. */
+int adamas_encode_query(const adamas_cache* cache, const void* q, int n_q_heads, uint16_t* out_ref,
+                        void* stream);
+
+/* score_all(q_code, cache, Metric::manhattan) per q-head (estimator.cpp:45-59):
+ * q_ref device uint16 [n_q_heads][16] -> device int32 [n_q_heads][seq_len]. */
+int adamas_score(const adamas_cache* cache, const uint16_t* q_ref, int n_q_heads, int32_t* scores,
+                 void* stream);
+
+/* top_k(scores, k) per row (estimator.cpp:75-90): the k smallest under the
+ * order (score, index), ascending indices. scores device int32 [n_rows][n]
+ * (values must lie in [0, 65535]); idx device int32 [n_rows][k]; entries past
+ * min(k, n) are set to -1. */
+int adamas_topk(const int32_t* scores, int n_rows, int64_t n, int64_t k, int32_t* idx, void* stream);
+
+/* sparse_attention(q, cache, sel) per q-head (attention.cpp:40-45 = gather,
+ * kv_cache.cpp:84-99, + full_attention, attention.cpp:8-38) in fp32:
+ * idx device int32 [n_q_heads][k] strictly increasing (-1 entries end a row);
+ * out device float32 [n_q_heads][128]; lse (optional, may be NULL) device
+ * float32 [n_q_heads][2] = (row max logit, sum of exp) for log-sum-exp merges. */
+int adamas_sparse_attention(const adamas_cache* cache, const void* q, int n_q_heads,
+                            const int32_t* idx, int64_t k, float* out, float* lse, void* stream);
+
+/* ---------------------------------------------------------------- decode step
+ * One Adamas decode step of one layer (Algorithm 1; sweep.cpp:87-98 then
+ * :225-226, with the cache update first): append the new
+ * token's (k, v) with its codes, encode q, scan every key code, select the
+ * top `budget` per q-head and attend over the selection.
+ * q: [n_q_heads][128]; k_new, v_new: [n_kv_heads][128]; out float32
+ * [n_q_heads][128]; idx (optional, may be NULL) int32 [n_q_heads][budget].
+ * Runs as one fused kernel launch. */
+int adamas_decode_step(adamas_cache* cache, const void* q, int n_q_heads, const void* k_new,
+                       const void* v_new, int64_t budget, float* out, int32_t* idx, void* stream);
+
+/* Same step for a batch of independent sequences (per-request caches with the
+ * same shape and dtype) in one launch: caches[i], q + i*n_q_heads*128, ...
+ * out + i*n_q_heads*128, idx + i*n_q_heads*budget. */
+int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const void* q, int n_q_heads,
+                               const void* k_new, const void* v_new, int64_t budget, float* out,
+                               int32_t* idx, void* stream);
+
+/* ---------------------------------------------------------------- host converters */
+
+/* Reference PackedCodes words <-> device bit-plane record (32 B), host memory,
+ * n vectors of 128 codes. Lossless both ways. */
+void adamas_codes_ref_to_planes(const uint16_t* ref, int64_t n, uint32_t* planes);
+void adamas_codes_planes_to_ref(const uint32_t* planes, int64_t n, uint16_t* ref);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

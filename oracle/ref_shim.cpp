@@ -1,0 +1,316 @@
+// ref_shim.cpp — extern "C" entry points over the UNMODIFIED reference library
+// (/root/reference/proj/src, compiled by oracle/Makefile into oracle/_ref/).
+//
+// TEST INFRASTRUCTURE ONLY: used to pin the C restatement (adamas_oracle.c),
+// to generate tests/golden/ fixtures, and as the reference CPU arm of bench.py
+// (cpu_baseline.kind = "reference"). Never linked into the product library.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+#include "adamas/attention.hpp"
+#include "adamas/common.hpp"
+#include "adamas/estimator.hpp"
+#include "adamas/hadamard.hpp"
+#include "adamas/kv_cache.hpp"
+#include "adamas/quantizer.hpp"
+#include "adamas/simd.hpp"
+
+using namespace adamas;
+
+namespace {
+
+// 0 ok, 1 ConfigError, 2 any other std::exception (adamas_cli.cpp:233-243 mapping).
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ConfigError&) {
+    return 1;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+// sweep.cpp:32-36 (encode with the Hadamard transform) — private there, so
+// restated here from the public operators it composes.
+CodeVector encode(std::span<const double> x, int bits) {
+  const RealVector t = fwht(x, {.dim = x.size()});
+  return bucketize(t, compute_thresholds(t, bits));
+}
+
+// Same integer synthetic generator as oracle/adamas_oracle.c:or_synth_value.
+uint64_t mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+float synth(uint64_t seed, uint64_t index) {
+  const uint64_t h = mix(seed ^ (index * 0xD1B54A32D192ED03ULL));
+  const int64_t s = (int64_t)(h & 0xFFFF) + (int64_t)((h >> 16) & 0xFFFF) +
+                    (int64_t)((h >> 32) & 0xFFFF) + (int64_t)(h >> 48);
+  return (float)((double)(s - 131070) / 37837.0);
+}
+float round_bf16(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);  // round to nearest even (finite inputs)
+  u &= 0xFFFF0000u;
+  float y;
+  std::memcpy(&y, &u, 4);
+  return y;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_simd_level() { return simd_level_name(active_simd_level()); }
+
+int ref_fwht(double* x, size_t n, int normalized) {
+  return guarded([&] {
+    auto y = fwht(std::span<const double>(x, n), {.dim = n, .normalized = normalized != 0});
+    std::copy(y.begin(), y.end(), x);
+  });
+}
+
+int ref_compute_thresholds(const double* x, size_t n, int bits, double* out) {
+  return guarded([&] {
+    auto t = compute_thresholds(std::span<const double>(x, n), bits);
+    std::copy(t.values.begin(), t.values.end(), out);
+  });
+}
+
+int ref_bucketize(const double* x, size_t n, const double* t, int bits, uint8_t* codes) {
+  return guarded([&] {
+    BucketThresholds th;
+    th.bits = bits;
+    th.values.assign(t, t + ((size_t{1} << bits) - 1));
+    auto c = bucketize(std::span<const double>(x, n), th);
+    std::copy(c.codes.begin(), c.codes.end(), codes);
+  });
+}
+
+int ref_pack(const uint8_t* codes, size_t n, int bits, uint16_t* words, size_t* nwords) {
+  return guarded([&] {
+    CodeVector c;
+    c.bits = bits;
+    c.codes.assign(codes, codes + n);
+    auto p = pack(c);
+    std::copy(p.words.begin(), p.words.end(), words);
+    *nwords = p.words.size();
+  });
+}
+
+int ref_encode_pack(const double* x, size_t d, uint16_t* words) {
+  return guarded([&] {
+    auto p = pack(encode(std::span<const double>(x, d), 2));
+    std::copy(p.words.begin(), p.words.end(), words);
+  });
+}
+
+uint32_t ref_manhattan_packed(const uint16_t* a, const uint16_t* b, size_t nwords) {
+  PackedCodes pa, pb;
+  pa.bits = pb.bits = 2;
+  pa.words.assign(a, a + nwords);
+  pb.words.assign(b, b + nwords);
+  pa.len = pb.len = nwords * 8;
+  return manhattan_packed(pa, pb);
+}
+
+void* ref_cache_new(size_t head_dim, int bits) {
+  try {
+    return new KvCache(head_dim, bits);
+  } catch (...) {
+    return nullptr;
+  }
+}
+void ref_cache_free(void* c) { delete static_cast<KvCache*>(c); }
+
+int ref_cache_update(void* c, const double* k, const double* v, const uint16_t* words) {
+  auto* cache = static_cast<KvCache*>(c);
+  return guarded([&] {
+    PackedCodes p;
+    p.bits = cache->bits();
+    p.words.assign(words, words + cache->words_per_code());
+    p.len = p.words.size() * (16u / unsigned(p.bits));
+    const size_t d = cache->head_dim();
+    cache->update(std::span<const double>(k, d), std::span<const double>(v, d), p);
+  });
+}
+
+size_t ref_cache_seq_len(void* c) { return static_cast<KvCache*>(c)->seq_len(); }
+
+void ref_cache_code_words(void* c, size_t i, uint16_t* out) {
+  auto w = static_cast<KvCache*>(c)->code_words(i);
+  std::copy(w.begin(), w.end(), out);
+}
+
+int ref_score_all(void* c, const uint16_t* qwords, int32_t* out) {
+  auto* cache = static_cast<KvCache*>(c);
+  return guarded([&] {
+    PackedCodes q;
+    q.bits = cache->bits();
+    q.words.assign(qwords, qwords + cache->words_per_code());
+    q.len = q.words.size() * (16u / unsigned(q.bits));
+    auto s = score_all(q, *cache, Metric::manhattan);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+
+size_t ref_top_k(const int32_t* scores, size_t n, size_t k, int64_t* idx) {
+  DistanceScores s(scores, scores + n);
+  auto sel = top_k(s, k);
+  for (size_t i = 0; i < sel.indices.size(); ++i) idx[i] = (int64_t)sel.indices[i];
+  return sel.indices.size();
+}
+
+int ref_sparse_attention(void* c, const double* q, const int64_t* idx, size_t nidx, double* out) {
+  auto* cache = static_cast<KvCache*>(c);
+  return guarded([&] {
+    SelectionResult sel;
+    sel.indices.assign(idx, idx + nidx);
+    auto o = sparse_attention(std::span<const double>(q, cache->head_dim()), *cache, sel);
+    std::copy(o.out.begin(), o.out.end(), out);
+  });
+}
+
+int ref_full_attention(const double* q, const double* K, const double* V, size_t rows, size_t d,
+                       double* out) {
+  return guarded([&] {
+    RealMatrix km(rows, d), vm(rows, d);
+    std::copy(K, K + rows * d, km.data().begin());
+    std::copy(V, V + rows * d, vm.data().begin());
+    auto o = full_attention(std::span<const double>(q, d), km, vm);
+    std::copy(o.out.begin(), o.out.end(), out);
+  });
+}
+
+// The reference decode step for one head (sweep.cpp:87-98 + :225-226).
+int ref_decode_head(void* c, const double* q, size_t budget, int64_t* idx, size_t* nidx,
+                    double* out) {
+  auto* cache = static_cast<KvCache*>(c);
+  return guarded([&] {
+    const std::span<const double> qs(q, cache->head_dim());
+    const auto qc = pack(encode(qs, 2));
+    const auto scores = score_all(qc, *cache, Metric::manhattan);
+    const auto sel = top_k(scores, budget);
+    const auto o = sparse_attention(qs, *cache, sel);
+    for (size_t i = 0; i < sel.indices.size(); ++i) idx[i] = (int64_t)sel.indices[i];
+    *nidx = sel.indices.size();
+    std::copy(o.out.begin(), o.out.end(), out);
+  });
+}
+
+// ---------------------------------------------------------------- CPU decode bench
+//
+// One "layer" = n_heads independent per-head caches of seq_len tokens (head_dim
+// d) built from the synthetic generator (bf16-rounded when bf16 != 0). A timed
+// decode step runs, for every head, the reference's own operators exactly as
+// its pipeline composes them: encode(k_new)+update (the append, Alg. 1 line 4),
+// then encode(q) -> score_all -> top_k -> sparse_attention. Heads are spread
+// over `threads` std::threads (operators are pure; heads are
+// independent). Returns the per-step wall times in us.
+struct RefLayer {
+  size_t d = 0, heads = 0, budget = 0;
+  uint64_t seed = 0;
+  bool bf16 = false;
+  std::vector<std::unique_ptr<KvCache>> caches;
+};
+
+void* ref_layer_build(size_t n_heads, size_t seq_len, size_t d, int bf16, uint64_t seed,
+                      int threads) {
+  auto* L = new RefLayer;
+  L->d = d;
+  L->heads = n_heads;
+  L->seed = seed;
+  L->bf16 = bf16 != 0;
+  L->caches.resize(n_heads);
+  auto work = [&](size_t h0, size_t h1) {
+    std::vector<double> k(d), v(d);
+    for (size_t h = h0; h < h1; ++h) {
+      auto c = std::make_unique<KvCache>(d, 2);
+      const uint64_t ks = seed * 1000003ULL + 2 * h + 1, vs = seed * 1000003ULL + 2 * h + 2;
+      for (size_t t = 0; t < seq_len; ++t) {
+        for (size_t j = 0; j < d; ++j) {
+          float a = synth(ks, t * d + j), b = synth(vs, t * d + j);
+          if (L->bf16) {
+            a = round_bf16(a);
+            b = round_bf16(b);
+          }
+          k[j] = a;
+          v[j] = b;
+        }
+        c->update(k, v, pack(encode(k, 2)));
+      }
+      L->caches[h] = std::move(c);
+    }
+  };
+  const int T = std::max(1, threads);
+  std::vector<std::thread> pool;
+  const size_t per = (n_heads + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    const size_t h0 = t * per, h1 = std::min(n_heads, h0 + per);
+    if (h0 < h1) pool.emplace_back(work, h0, h1);
+  }
+  for (auto& th : pool) th.join();
+  return L;
+}
+
+void ref_layer_free(void* p) { delete static_cast<RefLayer*>(p); }
+
+// Runs `steps` decode steps; step s appends one synthetic token per head and
+// then decodes one synthetic query per head. step_us[s] = wall time of step s.
+int ref_layer_decode(void* p, size_t budget, int threads, int steps, double* step_us) {
+  auto* L = static_cast<RefLayer*>(p);
+  const size_t d = L->d;
+  return guarded([&] {
+    for (int s = 0; s < steps; ++s) {
+      auto work = [&](size_t h0, size_t h1) {
+        std::vector<double> q(d), k(d), v(d);
+        for (size_t h = h0; h < h1; ++h) {
+          KvCache& c = *L->caches[h];
+          const uint64_t base = L->seed * 7919ULL + (uint64_t)s * 65537ULL + h;
+          for (size_t j = 0; j < d; ++j) {
+            float a = synth(base * 3 + 1, j), b = synth(base * 3 + 2, j), e = synth(base * 3 + 3, j);
+            if (L->bf16) {
+              a = round_bf16(a);
+              b = round_bf16(b);
+              e = round_bf16(e);
+            }
+            k[j] = a;
+            v[j] = b;
+            q[j] = e;
+          }
+          c.update(k, v, pack(encode(k, 2)));
+          const auto qc = pack(encode(q, 2));
+          const auto scores = score_all(qc, c, Metric::manhattan);
+          const auto sel = top_k(scores, budget);
+          const auto o = sparse_attention(q, c, sel);
+          if (!std::isfinite(o.out[0])) throw std::runtime_error("non-finite output");
+        }
+      };
+      const int T = std::max(1, threads);
+      const size_t per = (L->heads + T - 1) / T;
+      const auto t0 = std::chrono::steady_clock::now();
+      std::vector<std::thread> pool;
+      for (int t = 0; t < T; ++t) {
+        const size_t h0 = t * per, h1 = std::min(L->heads, h0 + per);
+        if (h0 < h1) pool.emplace_back(work, h0, h1);
+      }
+      for (auto& th : pool) th.join();
+      const auto t1 = std::chrono::steady_clock::now();
+      step_us[s] = std::chrono::duration<double, std::micro>(t1 - t0).count();
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+"""ctypes binding of the C ABI (include/adamas_b200.h).
+
+The product path is the CUDA library only: if libadamas_b200.so is missing or
+fails to load this module raises — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .build import LIB
+
+ADAMAS_OK = 0
+ADAMAS_ERR_CONFIG = 1
+ADAMAS_ERR_RUNTIME = 2
+ADAMAS_F32 = 0
+ADAMAS_BF16 = 1
+ADAMAS_STATUS_DEGENERATE = 1
+
+EXPORTED = [
+    "adamas_version", "adamas_last_error", "adamas_cache_create", "adamas_cache_destroy",
+    "adamas_cache_seq_len", "adamas_cache_truncate", "adamas_cache_buffers", "adamas_cache_status",
+    "adamas_cache_append", "adamas_cache_append_coded", "adamas_cache_codes_ref",
+    "adamas_encode_query", "adamas_score", "adamas_topk", "adamas_sparse_attention",
+    "adamas_decode_step", "adamas_decode_step_batched", "adamas_codes_ref_to_planes",
+    "adamas_codes_planes_to_ref",
+]
+
+
+class ConfigError(ValueError):
+    """Mirror of adamas::ConfigError (include/adamas/common.hpp:19-22)."""
+
+
+class AdamasRuntimeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB):
+        raise ImportError(f"{LIB} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB)
+    vp, i32, i64, sz = C.c_void_p, C.c_int, C.c_int64, C.c_size_t
+    L.adamas_version.restype = C.c_char_p
+    L.adamas_last_error.restype = C.c_char_p
+    L.adamas_cache_create.argtypes = [C.POINTER(vp), i32, i32, i32, i64, i32]
+    L.adamas_cache_destroy.argtypes = [vp]
+    L.adamas_cache_seq_len.argtypes = [vp, C.POINTER(i64)]
+    L.adamas_cache_truncate.argtypes = [vp, i64]
+    L.adamas_cache_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+    L.adamas_cache_status.argtypes = [vp, vp, C.POINTER(i32)]
+    L.adamas_cache_append.argtypes = [vp, vp, vp, i64, vp]
+    L.adamas_cache_append_coded.argtypes = [vp, vp, vp, vp, i64, vp]
+    L.adamas_cache_codes_ref.argtypes = [vp, i64, i64, vp, vp]
+    L.adamas_encode_query.argtypes = [vp, vp, i32, vp, vp]
+    L.adamas_score.argtypes = [vp, vp, i32, vp, vp]
+    L.adamas_topk.argtypes = [vp, i32, i64, i64, vp, vp]
+    L.adamas_sparse_attention.argtypes = [vp, vp, i32, vp, i64, vp, vp, vp]
+    L.adamas_decode_step.argtypes = [vp, vp, i32, vp, vp, i64, vp, vp, vp]
+    L.adamas_decode_step_batched.argtypes = [C.POINTER(vp), i32, vp, i32, vp, vp, i64, vp, vp, vp]
+    L.adamas_codes_ref_to_planes.argtypes = [vp, i64, vp]
+    L.adamas_codes_planes_to_ref.argtypes = [vp, i64, vp]
+    for name in EXPORTED:
+        if not hasattr(L, name):
+            raise ImportError(f"{LIB} does not export {name}")
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc == ADAMAS_OK:
+        return
+    msg = load().adamas_last_error().decode()
+    if rc == ADAMAS_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise AdamasRuntimeError(msg)

@@ -1,0 +1,465 @@
+// adamas_b200.cu — C ABI implementation (include/adamas_b200.h).
+// Host side owns the device cache arrays and launches the sm_100a kernels in
+// ops.cuh / fused_decode.cuh on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/adamas_b200.h"
+#include "fused_decode.cuh"
+#include "ops.cuh"
+
+using namespace adamas_dev;
+
+struct adamas_cache {
+  int n_kv = 0, head_dim = 0, bits = 0, dtype = 0, device = 0;
+  int64_t capacity = 0, seq_len = 0;
+  void* K = nullptr;
+  void* V = nullptr;
+  uint4* codes = nullptr;  // [n_kv][2 planes][capacity] x 16 B
+  int* status = nullptr;  // device sticky status word
+  // decode scratch (lazily grown)
+  int32_t* scores = nullptr;
+  size_t scores_elems = 0;
+  uint16_t* qref = nullptr;
+  int32_t* idx = nullptr;
+  size_t idx_elems = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define ADAMAS_CUDA(call)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(ADAMAS_ERR_RUNTIME, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ADAMAS_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+  return ADAMAS_OK;
+}
+
+size_t elem_size(int dtype) { return dtype == ADAMAS_BF16 ? 2 : 4; }
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int check_cache(const adamas_cache* c) {
+  if (c == nullptr) return fail(ADAMAS_ERR_CONFIG, "null cache handle");
+  return ADAMAS_OK;
+}
+
+int grow(int32_t** p, size_t* have, size_t need) {
+  if (*have >= need) return ADAMAS_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  ADAMAS_CUDA(cudaMalloc(p, need * sizeof(int32_t)));
+  *have = need;
+  return ADAMAS_OK;
+}
+
+template <typename T>
+int launch_append(adamas_cache* c, const void* keys, const void* values, const uint16_t* codes_ref,
+                  int64_t n_tokens, cudaStream_t s) {
+  const int64_t n_vec = n_tokens * c->n_kv;
+  const int64_t blocks_needed = (n_vec + kAppendWarps - 1) / kAppendWarps;
+  const int grid = (int)std::min<int64_t>(blocks_needed, (int64_t)sm_count() * 16);
+  if (codes_ref)
+    append_kernel<T, true><<<grid, kAppendWarps * 32, 0, s>>>(
+        (const T*)keys, (const T*)values, codes_ref, n_vec, c->n_kv, c->seq_len, c->capacity, (T*)c->K,
+        (T*)c->V, c->codes, c->status);
+  else
+    append_kernel<T, false><<<grid, kAppendWarps * 32, 0, s>>>(
+        (const T*)keys, (const T*)values, nullptr, n_vec, c->n_kv, c->seq_len, c->capacity, (T*)c->K,
+        (T*)c->V, c->codes, c->status);
+  return launch_check("append_kernel");
+}
+
+int do_append(adamas_cache* c, const void* keys, const void* values, const uint16_t* codes_ref,
+              int64_t n_tokens, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (n_tokens < 0) return fail(ADAMAS_ERR_CONFIG, "append: negative token count");
+  if (n_tokens == 0) return ADAMAS_OK;
+  if (!keys || !values) return fail(ADAMAS_ERR_CONFIG, "append: null key/value pointer");
+  if (c->seq_len + n_tokens > c->capacity)
+    return fail(ADAMAS_ERR_CONFIG, "append: cache capacity exceeded");
+  const int rc = c->dtype == ADAMAS_BF16
+                     ? launch_append<__nv_bfloat16>(c, keys, values, codes_ref, n_tokens, as_stream(stream))
+                     : launch_append<float>(c, keys, values, codes_ref, n_tokens, as_stream(stream));
+  if (rc == ADAMAS_OK) c->seq_len += n_tokens;
+  return rc;
+}
+
+int check_heads(const adamas_cache* c, int n_q) {
+  if (n_q < 1 || n_q % c->n_kv != 0)
+    return fail(ADAMAS_ERR_CONFIG, "n_q_heads must be a positive multiple of n_kv_heads");
+  return ADAMAS_OK;
+}
+
+
+// ----------------------------------------------------------------- fused launcher
+template <typename T, int G>
+int launch_fused_t(const FusedParams& prm, int C, size_t smem, cudaStream_t s) {
+  auto kern = fused_decode_kernel<T, G>;
+  static bool configured = false;
+  static size_t configured_smem = 0;
+  if (!configured || configured_smem < smem) {
+    ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+    configured_smem = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * C));
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ADAMAS_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  return ADAMAS_OK;
+}
+
+template <typename T>
+int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_fused_t<T, 1>(prm, C, smem, s);
+    case 2: return launch_fused_t<T, 2>(prm, C, smem, s);
+    case 4: return launch_fused_t<T, 4>(prm, C, smem, s);
+    case 8: return launch_fused_t<T, 8>(prm, C, smem, s);
+  }
+  return kFusedUnsupported;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// Chooses the cluster size C (CTAs per (sequence, kv-head) unit) and the
+// per-rank chunk, then launches. Returns kFusedUnsupported when the shape does
+// not fit the single-launch kernel (the caller composes operators instead).
+int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n_q, int dtype, const void* q,
+                        const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
+                        cudaStream_t s) {
+  const int G = n_q / n_kv;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return kFusedUnsupported;
+  if (n_seqs > kMaxSeqs || budget > (1 << 20)) return kFusedUnsupported;
+  int64_t s_max = 0;
+  for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + 1);
+  const int units = n_seqs * n_kv;
+  int C = env_int("ADAMAS_CLUSTER", 0);
+  if (C <= 0) {
+    C = 1;
+    while (C < 16 && units * C * 2 <= sm_count()) C *= 2;
+  }
+  const size_t smem_cap = 200 * 1024;
+  for (;;) {
+    int64_t chunk = (s_max + C - 1) / C;
+    chunk = (chunk + 255) / 256 * 256;
+    const int selcap = (int)std::min<int64_t>(budget, chunk);
+    const FusedSmem L(G, C, (int)chunk, selcap);
+    if (L.total <= smem_cap) {
+      FusedParams prm{};
+      prm.n_seqs = n_seqs;
+      prm.n_kv = n_kv;
+      prm.C = C;
+      prm.chunk = (int)chunk;
+      prm.budget = (int)budget;
+      prm.q = q;
+      prm.k_new = k_new;
+      prm.v_new = v_new;
+      prm.out = out;
+      prm.idx = idx;
+      prm.status = caches[0]->status;
+      for (int i = 0; i < n_seqs; ++i) {
+        prm.seq[i].codes = caches[i]->codes;
+        prm.seq[i].K = caches[i]->K;
+        prm.seq[i].V = caches[i]->V;
+        prm.seq[i].cap = caches[i]->capacity;
+        prm.seq[i].s_old = caches[i]->seq_len;
+      }
+      return dtype == ADAMAS_BF16 ? launch_fused_dtype<__nv_bfloat16>(prm, G, C, L.total, s)
+                                  : launch_fused_dtype<float>(prm, G, C, L.total, s);
+    }
+    if (C >= 16) return kFusedUnsupported;
+    C *= 2;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* adamas_version(void) { return "adamas-b200 0.1 (sm_100a)"; }
+
+const char* adamas_last_error(void) { return g_last_error.c_str(); }
+
+int adamas_cache_create(adamas_cache** out, int n_kv_heads, int head_dim, int bits, int64_t capacity,
+                        int kv_dtype) {
+  if (out == nullptr) return fail(ADAMAS_ERR_CONFIG, "null output handle");
+  *out = nullptr;
+  // KvCache ctor checks (kv_cache.cpp:33-34) plus the kernels' specialization.
+  if (head_dim == 0) return fail(ADAMAS_ERR_CONFIG, "KvCache: head_dim must be positive");
+  if (bits < 1 || bits > 3) return fail(ADAMAS_ERR_CONFIG, "KvCache: bits must be 1, 2, or 3");
+  if (head_dim != kHeadDim) return fail(ADAMAS_ERR_CONFIG, "adamas-b200 kernels specialize head_dim = 128");
+  if (bits != 2) return fail(ADAMAS_ERR_CONFIG, "adamas-b200 kernels specialize 2-bit codes");
+  if (n_kv_heads < 1) return fail(ADAMAS_ERR_CONFIG, "n_kv_heads must be positive");
+  if (capacity < 1 || capacity > (int64_t(1) << 31) - 1)
+    return fail(ADAMAS_ERR_CONFIG, "capacity must be in [1, 2^31)");
+  if (kv_dtype != ADAMAS_F32 && kv_dtype != ADAMAS_BF16) return fail(ADAMAS_ERR_CONFIG, "unknown kv dtype");
+  auto* c = new adamas_cache;
+  c->n_kv = n_kv_heads;
+  c->head_dim = head_dim;
+  c->bits = bits;
+  c->dtype = kv_dtype;
+  c->capacity = capacity;
+  cudaGetDevice(&c->device);
+  const size_t rows = (size_t)n_kv_heads * (size_t)capacity;
+  const size_t kv_bytes = rows * head_dim * elem_size(kv_dtype);
+  cudaError_t e = cudaMalloc(&c->K, kv_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->V, kv_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->codes, rows * 2 * sizeof(uint4));
+  if (e == cudaSuccess) e = cudaMalloc(&c->status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->status, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    adamas_cache_destroy(c);
+    return fail(ADAMAS_ERR_RUNTIME, std::string("cache allocation: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return ADAMAS_OK;
+}
+
+int adamas_cache_destroy(adamas_cache* c) {
+  if (c == nullptr) return ADAMAS_OK;
+  cudaFree(c->K);
+  cudaFree(c->V);
+  cudaFree(c->codes);
+  cudaFree(c->status);
+  cudaFree(c->scores);
+  cudaFree(c->qref);
+  cudaFree(c->idx);
+  delete c;
+  return ADAMAS_OK;
+}
+
+int adamas_cache_seq_len(const adamas_cache* c, int64_t* out) {
+  if (int rc = check_cache(c)) return rc;
+  if (!out) return fail(ADAMAS_ERR_CONFIG, "null output");
+  *out = c->seq_len;
+  return ADAMAS_OK;
+}
+
+int adamas_cache_truncate(adamas_cache* c, int64_t seq_len) {
+  if (int rc = check_cache(c)) return rc;
+  if (seq_len < 0 || seq_len > c->seq_len) return fail(ADAMAS_ERR_CONFIG, "truncate: out of range");
+  c->seq_len = seq_len;
+  return ADAMAS_OK;
+}
+
+int adamas_cache_buffers(const adamas_cache* c, void** keys, void** values, void** codes) {
+  if (int rc = check_cache(c)) return rc;
+  if (keys) *keys = c->K;
+  if (values) *values = c->V;
+  if (codes) *codes = c->codes;
+  return ADAMAS_OK;
+}
+
+int adamas_cache_status(adamas_cache* c, void* stream, int* status) {
+  if (int rc = check_cache(c)) return rc;
+  int h = 0;
+  ADAMAS_CUDA(cudaMemcpyAsync(&h, c->status, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream)));
+  ADAMAS_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), as_stream(stream)));
+  ADAMAS_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  if (status) *status = h;
+  return ADAMAS_OK;
+}
+
+int adamas_cache_append(adamas_cache* c, const void* keys, const void* values, int64_t n_tokens,
+                        void* stream) {
+  return do_append(c, keys, values, nullptr, n_tokens, stream);
+}
+
+int adamas_cache_append_coded(adamas_cache* c, const void* keys, const void* values,
+                              const uint16_t* codes_ref, int64_t n_tokens, void* stream) {
+  if (!codes_ref) return fail(ADAMAS_ERR_CONFIG, "append_coded: null codes");
+  return do_append(c, keys, values, codes_ref, n_tokens, stream);
+}
+
+int adamas_cache_codes_ref(const adamas_cache* c, int64_t start, int64_t n, uint16_t* out_ref,
+                           void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (start < 0 || n < 0 || start + n > c->seq_len) return fail(ADAMAS_ERR_CONFIG, "codes_ref: range");
+  if (n == 0) return ADAMAS_OK;
+  const int64_t vecs = n * c->n_kv;
+  const int grid = (int)((vecs + 7) / 8);
+  codes_to_ref_kernel<<<grid, 256, 0, as_stream(stream)>>>(c->codes, c->n_kv, c->capacity, start, n, out_ref);
+  return launch_check("codes_to_ref_kernel");
+}
+
+int adamas_encode_query(const adamas_cache* c, const void* q, int n_q, uint16_t* out_ref, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (n_q < 1 || !q || !out_ref) return fail(ADAMAS_ERR_CONFIG, "encode_query: bad arguments");
+  const int grid = (n_q + kAppendWarps - 1) / kAppendWarps;
+  if (c->dtype == ADAMAS_BF16)
+    encode_query_kernel<__nv_bfloat16><<<grid, kAppendWarps * 32, 0, as_stream(stream)>>>(
+        (const __nv_bfloat16*)q, n_q, out_ref, c->status);
+  else
+    encode_query_kernel<float><<<grid, kAppendWarps * 32, 0, as_stream(stream)>>>((const float*)q, n_q, out_ref,
+                                                                                  c->status);
+  return launch_check("encode_query_kernel");
+}
+
+int adamas_score(const adamas_cache* c, const uint16_t* q_ref, int n_q, int32_t* scores, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (!q_ref || !scores) return fail(ADAMAS_ERR_CONFIG, "score: null pointer");
+  if (c->seq_len == 0) return ADAMAS_OK;  // estimator: empty cache -> empty scores
+  const int64_t per_block = (int64_t)kScoreThreads * kScoreTokensPerThread;
+  dim3 grid((unsigned)((c->seq_len + per_block - 1) / per_block), (unsigned)n_q);
+  score_kernel<<<grid, kScoreThreads, 0, as_stream(stream)>>>(c->codes, c->capacity, c->seq_len, n_q / c->n_kv,
+                                                             q_ref, scores);
+  return launch_check("score_kernel");
+}
+
+int adamas_topk(const int32_t* scores, int n_rows, int64_t n, int64_t k, int32_t* idx, void* stream) {
+  if (n_rows < 1 || n < 0 || k < 0) return fail(ADAMAS_ERR_CONFIG, "topk: bad sizes");
+  if (k == 0) return ADAMAS_OK;
+  if (!idx || (n > 0 && !scores)) return fail(ADAMAS_ERR_CONFIG, "topk: null pointer");
+  if (n > (int64_t(1) << 31) - 1) return fail(ADAMAS_ERR_CONFIG, "topk: n too large");
+  static int* dummy_status = nullptr;
+  if (!dummy_status) ADAMAS_CUDA(cudaMalloc(&dummy_status, sizeof(int)));
+  topk_kernel<<<n_rows, kTopkThreads, 0, as_stream(stream)>>>(scores, n, k, idx, dummy_status);
+  return launch_check("topk_kernel");
+}
+
+int adamas_sparse_attention(const adamas_cache* c, const void* q, int n_q, const int32_t* idx, int64_t k,
+                            float* out, float* lse, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (k < 1) return fail(ADAMAS_ERR_CONFIG, "sparse_attention: empty selection");
+  if (!q || !idx || !out) return fail(ADAMAS_ERR_CONFIG, "sparse_attention: null pointer");
+  const int group = n_q / c->n_kv;
+  if (c->dtype == ADAMAS_BF16)
+    attend_kernel<__nv_bfloat16><<<n_q, kAttnWarps * 32, 0, as_stream(stream)>>>(
+        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, idx,
+        k, out, lse);
+  else
+    attend_kernel<float><<<n_q, kAttnWarps * 32, 0, as_stream(stream)>>>(
+        (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, idx, k, out, lse);
+  return launch_check("attend_kernel");
+}
+
+int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const void* q, int n_q,
+                               const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
+                               void* stream) {
+  if (!caches || n_seqs < 1) return fail(ADAMAS_ERR_CONFIG, "decode: no caches");
+  adamas_cache* c0 = caches[0];
+  if (int rc = check_cache(c0)) return rc;
+  if (int rc = check_heads(c0, n_q)) return rc;
+  if (budget < 1) return fail(ADAMAS_ERR_CONFIG, "decode: budget must be >= 1 (empty selection)");
+  if (!q || !k_new || !v_new || !out) return fail(ADAMAS_ERR_CONFIG, "decode: null pointer");
+  for (int i = 0; i < n_seqs; ++i) {
+    adamas_cache* c = caches[i];
+    if (int rc = check_cache(c)) return rc;
+    if (c->n_kv != c0->n_kv || c->dtype != c0->dtype)
+      return fail(ADAMAS_ERR_CONFIG, "decode: batched caches differ in shape");
+    if (c->seq_len + 1 > c->capacity) return fail(ADAMAS_ERR_CONFIG, "decode: cache capacity exceeded");
+  }
+  const size_t es = elem_size(c0->dtype);
+  const size_t q_stride = (size_t)n_q * kHeadDim * es, kv_stride = (size_t)c0->n_kv * kHeadDim * es;
+  int rc = env_int("ADAMAS_NO_FUSED", 0)
+               ? kFusedUnsupported
+               : fused_decode_launch(caches, n_seqs, c0->n_kv, n_q, c0->dtype, q, k_new, v_new, budget, out, idx,
+                                     as_stream(stream));
+  if (rc == kFusedUnsupported) {
+    // Operator composition (same semantics, several launches).
+    for (int i = 0; i < n_seqs; ++i) {
+      adamas_cache* c = caches[i];
+      const char* qi = (const char*)q + i * q_stride;
+      const char* ki = (const char*)k_new + i * kv_stride;
+      const char* vi = (const char*)v_new + i * kv_stride;
+      float* oi = out + (size_t)i * n_q * kHeadDim;
+      if ((rc = do_append(c, ki, vi, nullptr, 1, stream))) return rc;
+      if ((rc = grow(&c->scores, &c->scores_elems, (size_t)n_q * c->seq_len))) return rc;
+      if (!c->qref) ADAMAS_CUDA(cudaMalloc(&c->qref, 4096 * 16 * sizeof(uint16_t)));
+      if (n_q > 4096) return fail(ADAMAS_ERR_CONFIG, "decode: too many heads");
+      int32_t* id = idx ? idx + (size_t)i * n_q * budget : nullptr;
+      if (!id) {
+        if ((rc = grow(&c->idx, &c->idx_elems, (size_t)n_q * budget))) return rc;
+        id = c->idx;
+      }
+      if ((rc = adamas_encode_query(c, qi, n_q, c->qref, stream))) return rc;
+      if ((rc = adamas_score(c, c->qref, n_q, c->scores, stream))) return rc;
+      if ((rc = adamas_topk(c->scores, n_q, c->seq_len, budget, id, stream))) return rc;
+      if ((rc = adamas_sparse_attention(c, qi, n_q, id, budget, oi, nullptr, stream))) return rc;
+    }
+    return ADAMAS_OK;
+  }
+  if (rc != ADAMAS_OK) return rc;
+  for (int i = 0; i < n_seqs; ++i) caches[i]->seq_len += 1;
+  return ADAMAS_OK;
+}
+
+int adamas_decode_step(adamas_cache* c, const void* q, int n_q, const void* k_new, const void* v_new,
+                       int64_t budget, float* out, int32_t* idx, void* stream) {
+  adamas_cache* arr[1] = {c};
+  return adamas_decode_step_batched(arr, 1, q, n_q, k_new, v_new, budget, out, idx, stream);
+}
+
+void adamas_codes_ref_to_planes(const uint16_t* ref, int64_t n, uint32_t* planes) {
+  for (int64_t v = 0; v < n; ++v) {
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(ref + v * 16);
+    uint32_t* p = planes + v * 8;
+    for (int w = 0; w < 8; ++w) p[w] = 0;
+    for (int e = 0; e < kHeadDim; ++e) {
+      const uint32_t code = (b[e / 4] >> (2 * (e % 4))) & 3u;
+      p[e % 4] |= (code & 1u) << (e / 4);
+      p[4 + e % 4] |= (code >> 1) << (e / 4);
+    }
+  }
+}
+
+void adamas_codes_planes_to_ref(const uint32_t* planes, int64_t n, uint16_t* ref) {
+  for (int64_t v = 0; v < n; ++v) {
+    const uint32_t* p = planes + v * 8;
+    uint8_t* b = reinterpret_cast<uint8_t*>(ref + v * 16);
+    for (int i = 0; i < 32; ++i) b[i] = 0;
+    for (int e = 0; e < kHeadDim; ++e) {
+      const uint32_t code = ((p[e % 4] >> (e / 4)) & 1u) | (((p[4 + e % 4] >> (e / 4)) & 1u) << 1);
+      b[e / 4] |= (uint8_t)(code << (2 * (e % 4)));
+    }
+  }
+}
+
+}  // extern "C"

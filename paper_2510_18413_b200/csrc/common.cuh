@@ -1,0 +1,208 @@
+// common.cuh — device building blocks shared by every Adamas kernel (sm_100a).
+//
+// Code layout in HBM ("bit-plane", 32 B per token per kv-head at d = 128):
+//   two plane arrays per kv-head, each [capacity] x 16 B:
+//     lo plane of token t of kv-head h at planes[(2h + 0) * capacity + t]
+//     hi plane                         at planes[(2h + 1) * capacity + t]
+//   Element e (0..127) of the transformed key sits at bit (e / 4) of word
+//   e % 4 of the lo plane (low code bit) and of the hi plane (high bit).
+//   Separate planes make every per-lane 16-byte access (global or the
+//   bulk-copied shared-memory stage) contiguous across a warp.
+// This is the reference PackedCodes (quantizer.hpp:44-50: element i at bits
+// [2(i%8), 2(i%8)+2) of u16 word i/8) with the bits transposed into planes, so
+// the Manhattan distance becomes ~3 LOP3 + 2 POPC per 32 elements instead of
+// the reference's nibble SWAR (kernels_scalar.cpp:41-70). Layout is an
+// implementation freedom; the integer results are identical.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace adamas_dev {
+
+constexpr int kHeadDim = 128;
+constexpr uint32_t kFull = 0xffffffffu;
+// k_inv_sqrt2 (reference kernels_impl.hpp:10) and kQ28 (quantizer.cpp:13).
+constexpr double kInvSqrt2 = 0.70710678118654752440;
+constexpr double kQ28 = 0.6744897501960817432;
+
+// Sticky status bits (C-ABI ADAMAS_STATUS_*).
+constexpr int kStatusDegenerate = 1;  // zero or non-finite vector (quantizer.cpp:46-47)
+
+struct __align__(32) Code {
+  uint32_t lo[4];
+  uint32_t hi[4];
+};
+
+// Query-side precomputation for the distance: X = lo ^ hi.
+struct QCode {
+  uint32_t lo[4], hi[4], x[4];
+};
+
+__device__ __forceinline__ QCode make_qcode(const Code& c) {
+  QCode q;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    q.lo[w] = c.lo[w];
+    q.hi[w] = c.hi[w];
+    q.x[w] = c.lo[w] ^ c.hi[w];
+  }
+  return q;
+}
+
+// Sum over the 128 elements of |q_e - k_e| for 2-bit codes in bit planes.
+// Per element with a = 2ah + al, b = 2bh + bl:  |a - b| = L + 2A where
+// L = al ^ bl and A = (ah ^ bh) & ~(L & (al ^ ah)). Checked exhaustively over
+// all 16 (a, b) pairs in tests/test_layout.py.
+__device__ __forceinline__ uint32_t l1_distance(const QCode& q, const uint32_t klo[4],
+                                                const uint32_t khi[4]) {
+  uint32_t d = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t L = q.lo[w] ^ klo[w];
+    const uint32_t A = (q.hi[w] ^ khi[w]) & ~(L & q.x[w]);
+    d += __popc(L) + 2u * __popc(A);
+  }
+  return d;
+}
+
+// Streaming 128-bit load (no L1 allocation).
+__device__ __forceinline__ void ld_plane_nc(const uint4* p, uint32_t w[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+               : "l"(p));
+}
+
+// ---------------------------------------------------------------------------
+// Element loads: lane l owns elements 4l .. 4l+3 of a 128-vector.
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+  __device__ static __forceinline__ void load4(const float* p, float v[4]) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+  __device__ static __forceinline__ void store4(float* p, const float v[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+  __device__ static __forceinline__ void load4(const __nv_bfloat16* p, float v[4]) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = __uint_as_float(u.x << 16);
+    v[1] = __uint_as_float(u.x & 0xffff0000u);
+    v[2] = __uint_as_float(u.y << 16);
+    v[3] = __uint_as_float(u.y & 0xffff0000u);
+  }
+  __device__ static __forceinline__ void load4_raw(const __nv_bfloat16* p, uint2& u) {
+    u = *reinterpret_cast<const uint2*>(p);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Encoder: normalized FWHT (kernels_scalar.cpp:11-22), RMS thresholds
+// (quantizer.cpp:40-64), strict-'>' bucketize (quantizer.cpp:74-85) and the
+// bit-plane pack, for one 128-vector held 4 elements per lane across a warp.
+// All arithmetic is fp64 with explicit _rn intrinsics (no FMA contraction),
+// the butterflies in the reference's stage order and the sum of squares in
+// index order, so the codes are bit-identical to the reference's.
+// `sq` is a 128-double per-warp scratch in shared memory.
+// Returns false (and zero codes) for a zero / non-finite vector.
+__device__ __forceinline__ bool encode128_warp(const float in[4], double* sq, Code& out) {
+  const int lane = threadIdx.x & 31;
+  double x[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) x[j] = (double)in[j];
+  // stage h = 1: (0,1), (2,3) within the lane
+  {
+    const double a0 = x[0], b0 = x[1], a1 = x[2], b1 = x[3];
+    x[0] = __dmul_rn(__dadd_rn(a0, b0), kInvSqrt2);
+    x[1] = __dmul_rn(__dsub_rn(a0, b0), kInvSqrt2);
+    x[2] = __dmul_rn(__dadd_rn(a1, b1), kInvSqrt2);
+    x[3] = __dmul_rn(__dsub_rn(a1, b1), kInvSqrt2);
+  }
+  // stage h = 2: (0,2), (1,3) within the lane
+  {
+    const double a0 = x[0], b0 = x[2], a1 = x[1], b1 = x[3];
+    x[0] = __dmul_rn(__dadd_rn(a0, b0), kInvSqrt2);
+    x[2] = __dmul_rn(__dsub_rn(a0, b0), kInvSqrt2);
+    x[1] = __dmul_rn(__dadd_rn(a1, b1), kInvSqrt2);
+    x[3] = __dmul_rn(__dsub_rn(a1, b1), kInvSqrt2);
+  }
+  // stages h = 4 .. 64: partner lane at distance h / 4
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double p = __shfl_xor_sync(kFull, x[j], m);
+      // lower element j: (a + b) c with a = mine; upper: (a - b) c with a = partner
+      x[j] = upper ? __dmul_rn(__dsub_rn(p, x[j]), kInvSqrt2)
+                   : __dmul_rn(__dadd_rn(x[j], p), kInvSqrt2);
+    }
+  }
+  // sum of squares in index order 0..127 (quantizer.cpp:43-44)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sq[lane * 4 + j] = __dmul_rn(x[j], x[j]);
+  __syncwarp();
+  double sumsq = 0.0;
+#pragma unroll 16
+  for (int e = 0; e < kHeadDim; ++e) sumsq = __dadd_rn(sumsq, sq[e]);
+  __syncwarp();
+  const double sigma = __dsqrt_rn(__ddiv_rn(sumsq, (double)kHeadDim));
+  const bool ok = isfinite(sigma) && sigma != 0.0;
+  const double t_hi = __dmul_rn(kQ28, sigma);
+  const double t_lo = __dmul_rn(-kQ28, sigma);
+  uint32_t code[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    code[j] = ok ? (uint32_t)(x[j] > t_lo) + (uint32_t)(x[j] > 0.0) + (uint32_t)(x[j] > t_hi) : 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    out.lo[j] = __ballot_sync(kFull, code[j] & 1u);
+    out.hi[j] = __ballot_sync(kFull, code[j] >> 1);
+  }
+  return ok;
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk-copy (TMA engine, non-tensor) helpers.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(kFull, v, m);
+  return v;
+}
+
+}  // namespace adamas_dev

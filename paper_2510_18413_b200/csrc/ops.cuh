@@ -1,0 +1,336 @@
+// ops.cuh — operator-level kernels behind the C ABI (one kernel per reference
+// operator): encode+append, query encode, score_all, top_k, sparse_attention.
+// The fused single-launch decode step lives in fused_decode.cuh.
+#pragma once
+#include "common.cuh"
+
+namespace adamas_dev {
+
+// ----------------------------------------------------------------- raw moves
+template <typename T>
+struct Raw4;  // four consecutive elements as one vector register
+template <>
+struct Raw4<float> {
+  using V = float4;
+  __device__ static __forceinline__ V load(const float* p) { return *reinterpret_cast<const float4*>(p); }
+  __device__ static __forceinline__ void store(float* p, V v) { *reinterpret_cast<float4*>(p) = v; }
+  __device__ static __forceinline__ void to_float(V v, float f[4]) {
+    f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+  }
+};
+template <>
+struct Raw4<__nv_bfloat16> {
+  using V = uint2;
+  __device__ static __forceinline__ V load(const __nv_bfloat16* p) { return *reinterpret_cast<const uint2*>(p); }
+  __device__ static __forceinline__ void store(__nv_bfloat16* p, V v) { *reinterpret_cast<uint2*>(p) = v; }
+  __device__ static __forceinline__ void to_float(V v, float f[4]) {
+    f[0] = __uint_as_float(v.x << 16);
+    f[1] = __uint_as_float(v.x & 0xffff0000u);
+    f[2] = __uint_as_float(v.y << 16);
+    f[3] = __uint_as_float(v.y & 0xffff0000u);
+  }
+};
+
+// Reference-layout code byte of lane l (elements 4l..4l+3) -> four 2-bit codes.
+// (PackedCodes words are little-endian u16, so byte l of the 32-byte row holds
+// elements 4l..4l+3 at bit offsets 0, 2, 4, 6.)
+__device__ __forceinline__ void planes_from_ref_byte(uint32_t byte, Code& out) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t c = (byte >> (2 * j)) & 3u;
+    out.lo[j] = __ballot_sync(kFull, c & 1u);
+    out.hi[j] = __ballot_sync(kFull, c >> 1);
+  }
+}
+__device__ __forceinline__ uint32_t ref_byte_from_planes(const Code& c, int lane) {
+  uint32_t b = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t code = ((c.lo[j] >> lane) & 1u) | (((c.hi[j] >> lane) & 1u) << 1);
+    b |= code << (2 * j);
+  }
+  return b;
+}
+__device__ __forceinline__ uint32_t ref_byte_from_codes(const uint32_t code[4]) {
+  return code[0] | (code[1] << 2) | (code[2] << 4) | (code[3] << 6);
+}
+
+// planes: the kv-head's lo plane base; the hi plane is `cap` records later.
+__device__ __forceinline__ void store_code(uint4* planes, int64_t cap, int64_t t, const Code& c) {
+  planes[t] = make_uint4(c.lo[0], c.lo[1], c.lo[2], c.lo[3]);
+  planes[cap + t] = make_uint4(c.hi[0], c.hi[1], c.hi[2], c.hi[3]);
+}
+__device__ __forceinline__ Code load_code(const uint4* planes, int64_t cap, int64_t t) {
+  const uint4 a = planes[t], b = planes[cap + t];
+  Code c;
+  c.lo[0] = a.x; c.lo[1] = a.y; c.lo[2] = a.z; c.lo[3] = a.w;
+  c.hi[0] = b.x; c.hi[1] = b.y; c.hi[2] = b.z; c.hi[3] = b.w;
+  return c;
+}
+
+// ----------------------------------------------------------------- append
+// One warp per (token, kv-head) vector: copy k and v into the cache rows and
+// write the key's code (encoded here, or converted from reference words).
+constexpr int kAppendWarps = 8;
+
+template <typename T, bool kCoded>
+__global__ void __launch_bounds__(kAppendWarps * 32)
+append_kernel(const T* __restrict__ keys, const T* __restrict__ values,
+              const uint16_t* __restrict__ codes_ref, int64_t n_vec, int n_kv, int64_t seq0,
+              int64_t cap, T* __restrict__ K, T* __restrict__ V, uint4* __restrict__ codes,
+              int* __restrict__ status) {
+  __shared__ double sq[kAppendWarps][kHeadDim];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t stride = (int64_t)gridDim.x * kAppendWarps;
+  for (int64_t vec = (int64_t)blockIdx.x * kAppendWarps + warp; vec < n_vec; vec += stride) {
+    const int64_t t = vec / n_kv;
+    const int h = (int)(vec % n_kv);
+    const int64_t row = (int64_t)h * cap + seq0 + t;
+    const auto kr = Raw4<T>::load(keys + vec * kHeadDim + lane * 4);
+    const auto vr = Raw4<T>::load(values + vec * kHeadDim + lane * 4);
+    Raw4<T>::store(K + row * kHeadDim + lane * 4, kr);
+    Raw4<T>::store(V + row * kHeadDim + lane * 4, vr);
+    Code c;
+    if constexpr (kCoded) {
+      const uint32_t byte = reinterpret_cast<const uint8_t*>(codes_ref + vec * 16)[lane];
+      planes_from_ref_byte(byte, c);
+    } else {
+      float f[4];
+      Raw4<T>::to_float(kr, f);
+      const bool ok = encode128_warp(f, sq[warp], c);
+      if (!ok && lane == 0) atomicOr(status, kStatusDegenerate);
+    }
+    if (lane == 0) store_code(codes + (int64_t)h * 2 * cap, cap, seq0 + t, c);
+  }
+}
+
+// ----------------------------------------------------------------- query encode
+template <typename T>
+__global__ void __launch_bounds__(kAppendWarps * 32)
+encode_query_kernel(const T* __restrict__ q, int n_q, uint16_t* __restrict__ out_ref,
+                    int* __restrict__ status) {
+  __shared__ double sq[kAppendWarps][kHeadDim];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = blockIdx.x * kAppendWarps + warp;
+  if (h >= n_q) return;
+  float f[4];
+  Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)h * kHeadDim + lane * 4), f);
+  Code c;
+  const bool ok = encode128_warp(f, sq[warp], c);
+  if (!ok && lane == 0) atomicOr(status, kStatusDegenerate);
+  reinterpret_cast<uint8_t*>(out_ref + (int64_t)h * 16)[lane] = (uint8_t)ref_byte_from_planes(c, lane);
+}
+
+// ----------------------------------------------------------------- codes out
+__global__ void codes_to_ref_kernel(const uint4* __restrict__ codes, int n_kv, int64_t cap,
+                                    int64_t start, int64_t n, uint16_t* __restrict__ out_ref) {
+  const int lane = threadIdx.x & 31;
+  const int64_t vec = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (vec >= (int64_t)n_kv * n) return;
+  const int h = (int)(vec / n);
+  const int64_t t = vec % n;
+  const Code c = load_code(codes + (int64_t)h * 2 * cap, cap, start + t);
+  reinterpret_cast<uint8_t*>(out_ref + vec * 16)[lane] = (uint8_t)ref_byte_from_planes(c, lane);
+}
+
+// ----------------------------------------------------------------- score_all
+constexpr int kScoreThreads = 256;
+constexpr int kScoreTokensPerThread = 4;
+
+__global__ void __launch_bounds__(kScoreThreads)
+score_kernel(const uint4* __restrict__ codes, int64_t cap, int64_t S, int group,
+             const uint16_t* __restrict__ q_ref, int32_t* __restrict__ scores) {
+  __shared__ Code qs;
+  const int hq = blockIdx.y;
+  const int hk = hq / group;
+  if (threadIdx.x < 32) {
+    const uint32_t byte = reinterpret_cast<const uint8_t*>(q_ref + (int64_t)hq * 16)[threadIdx.x];
+    Code c;
+    planes_from_ref_byte(byte, c);
+    if (threadIdx.x == 0) qs = c;
+  }
+  __syncthreads();
+  const QCode q = make_qcode(qs);
+  const uint4* lo_plane = codes + (int64_t)hk * 2 * cap;
+  const uint4* hi_plane = lo_plane + cap;
+  const int64_t t0 = (int64_t)blockIdx.x * kScoreThreads * kScoreTokensPerThread + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < kScoreTokensPerThread; ++i) {
+    const int64_t t = t0 + (int64_t)i * kScoreThreads;
+    if (t < S) {
+      uint32_t lo[4], hi[4];
+      ld_plane_nc(lo_plane + t, lo);
+      ld_plane_nc(hi_plane + t, hi);
+      scores[(int64_t)hq * S + t] = (int32_t)l1_distance(q, lo, hi);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- top_k
+// One CTA per row: histogram of the (small, non-negative) scores, threshold
+// T = smallest value whose cumulative count reaches k, then an order-preserving
+// compaction of {score < T} plus the first (k - #below) indices with score == T
+// (estimator.cpp:81-88: ties resolve toward the smaller index). The output is
+// ascending by construction; no sort.
+constexpr int kTopkThreads = 1024;
+constexpr int kTopkBins = 1024;
+
+// Exclusive prefix of a 0/1 flag over the CTA in thread order; returns the
+// prefix and writes the CTA total to *total. `scratch` holds 32 ints.
+__device__ __forceinline__ int block_flag_scan(bool flag, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t b = __ballot_sync(kFull, flag);
+  const int in_warp = __popc(b & ((1u << lane) - 1u));
+  if (lane == 0) scratch[warp] = __popc(b);
+  __syncthreads();
+  int before = 0, sum = 0;
+  for (int w = 0; w < nwarps; ++w) {
+    const int v = scratch[w];
+    before += (w < warp) ? v : 0;
+    sum += v;
+  }
+  __syncthreads();
+  *total = sum;
+  return before + in_warp;
+}
+
+__global__ void __launch_bounds__(kTopkThreads)
+topk_kernel(const int32_t* __restrict__ scores, int64_t n, int64_t k, int32_t* __restrict__ idx,
+            int* __restrict__ status) {
+  __shared__ int hist[kTopkBins];
+  __shared__ int scratch[32];
+  __shared__ int s_T, s_need;
+  const int row = blockIdx.x;
+  const int32_t* s = scores + (int64_t)row * n;
+  int32_t* out = idx + (int64_t)row * k;
+  const int64_t keep = k < n ? k : n;
+  for (int64_t i = keep + threadIdx.x; i < k; i += blockDim.x) out[i] = -1;
+  if (k >= n) {  // estimator.cpp:80 — everything, in order
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = (int32_t)i;
+    return;
+  }
+  if (k == 0) return;
+  for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    int v = s[i];
+    if (v < 0 || v >= kTopkBins) {
+      atomicOr(status, 2);
+      v = v < 0 ? 0 : kTopkBins - 1;
+    }
+    atomicAdd(&hist[v], 1);
+  }
+  __syncthreads();
+  // inclusive scan of the histogram (one bin per thread)
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int v = hist[threadIdx.x];
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const int o = __shfl_up_sync(kFull, v, m);
+      if (lane >= m) v += o;
+    }
+    if (lane == 31) scratch[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int w = scratch[lane];
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const int o = __shfl_up_sync(kFull, w, m);
+        if (lane >= m) w += o;
+      }
+      scratch[lane] = w;
+    }
+    __syncthreads();
+    const int cum = v + (warp > 0 ? scratch[warp - 1] : 0);
+    const int prev = cum - hist[threadIdx.x];
+    if (prev < k && cum >= k) {
+      s_T = threadIdx.x;
+      s_need = (int)(k - prev);
+    }
+    __syncthreads();
+  }
+  const int T = s_T;
+  const int need = s_need;
+  int eq_seen = 0, taken = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int v = i < n ? s[i] : 0x7fffffff;
+    const bool eq = (i < n) && v == T;
+    int eq_total;
+    const int eq_before = eq_seen + block_flag_scan(eq, scratch, &eq_total);
+    const bool take = (i < n) && (v < T || (eq && eq_before < need));
+    int take_total;
+    const int pos = taken + block_flag_scan(take, scratch, &take_total);
+    if (take) out[pos] = (int32_t)i;
+    eq_seen += eq_total;
+    taken += take_total;
+    if (taken >= keep) break;
+  }
+}
+
+// ----------------------------------------------------------------- sparse attention
+// One CTA per q-head; each warp walks rows warp, warp+8, ... with an online
+// softmax over its rows (fp32), then the eight (m, l, o) partials are merged.
+constexpr int kAttnWarps = 8;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <typename T>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
+              const T* __restrict__ q, const int32_t* __restrict__ idx, int64_t k,
+              float* __restrict__ out, float* __restrict__ lse) {
+  __shared__ float sm[kAttnWarps], sl[kAttnWarps];
+  __shared__ float so[kAttnWarps][kHeadDim];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hq = blockIdx.x, hk = hq / group;
+  float qf[4];
+  Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)hq * kHeadDim + lane * 4), qf);
+  // logits in log2 units: q.k / sqrt(128) * log2(e)
+  const float scale = 0.088388347648318440f * kLog2e;
+  const int32_t* row_idx = idx + (int64_t)hq * k;
+  const T* Kh = K + (int64_t)hk * cap * kHeadDim;
+  const T* Vh = V + (int64_t)hk * cap * kHeadDim;
+  float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = warp; r < k; r += kAttnWarps) {
+    const int32_t t = row_idx[r];
+    if (t < 0) break;
+    float kf[4], vf[4];
+    Raw4<T>::to_float(Raw4<T>::load(Kh + (int64_t)t * kHeadDim + lane * 4), kf);
+    Raw4<T>::to_float(Raw4<T>::load(Vh + (int64_t)t * kHeadDim + lane * 4), vf);
+    float dot = qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3];
+    dot = warp_sum(dot) * scale;
+    const float mn = fmaxf(m, dot);
+    const float corr = exp2f(m - mn);
+    const float p = exp2f(dot - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = o[j] * corr + p * vf[j];
+    m = mn;
+  }
+  if (lane == 0) { sm[warp] = m; sl[warp] = l; }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) so[warp][lane * 4 + j] = o[j];
+  __syncthreads();
+  if (warp == 0) {
+    float M = -INFINITY;
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm[w]);
+    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int w = 0; w < kAttnWarps; ++w) {
+      if (sl[w] == 0.f) continue;
+      const float c = exp2f(sm[w] - M);
+      L += sl[w] * c;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += so[w][lane * 4 + j] * c;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    float4 res = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    *reinterpret_cast<float4*>(out + (int64_t)hq * kHeadDim + lane * 4) = res;
+    if (lse != nullptr && lane == 0) {
+      lse[2 * hq] = M / kLog2e;  // natural-log units
+      lse[2 * hq + 1] = L;
+    }
+  }
+}
+
+}  // namespace adamas_dev

@@ -1,0 +1,101 @@
+"""CPU: the C ABI library loads, exports every symbol include/adamas_b200.h
+declares, rejects bad configurations like the reference (ConfigError) without
+touching the device, and the host layout converters are lossless."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle.bindings import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_2510_18413_b200 import build
+    build.build()
+    from paper_2510_18413_b200._lib import load
+    return load()
+
+
+def test_exports_every_declared_symbol():
+    L = _lib()
+    header = open(os.path.join(ROOT, "include", "adamas_b200.h")).read()
+    names = set(re.findall(r"\b(adamas_[a-z0-9_]+)\s*\(", header))
+    assert len(names) >= 19
+    for n in sorted(names):
+        assert hasattr(L, n), n
+    assert b"sm_100a" in L.adamas_version()
+
+
+def test_cache_create_rejects_like_kv_cache_ctor():
+    L = _lib()
+    h = C.c_void_p()
+    # kv_cache.cpp:33-34 and the sm_100a specialization: ConfigError (1)
+    assert L.adamas_cache_create(C.byref(h), 1, 0, 2, 16, 0) == 1
+    assert L.adamas_cache_create(C.byref(h), 1, 128, 0, 16, 0) == 1
+    assert L.adamas_cache_create(C.byref(h), 1, 128, 4, 16, 0) == 1
+    assert L.adamas_cache_create(C.byref(h), 1, 64, 2, 16, 0) == 1
+    assert b"128" in L.adamas_last_error()
+    assert L.adamas_cache_create(C.byref(h), 1, 128, 1, 16, 0) == 1
+    assert L.adamas_cache_create(C.byref(h), 0, 128, 2, 16, 0) == 1
+    assert L.adamas_cache_create(C.byref(h), 1, 128, 2, 0, 0) == 1
+    assert L.adamas_cache_create(C.byref(h), 1, 128, 2, 16, 7) == 1
+    assert L.adamas_topk(None, 0, 10, 1, None, None) == 1
+
+
+def test_plane_converters_roundtrip(oracle):
+    L = _lib()
+    rng = np.random.default_rng(0)
+    ref = rng.integers(0, 65536, (257, 16)).astype(np.uint16)
+    planes = np.zeros((257, 8), np.uint32)
+    back = np.zeros_like(ref)
+    L.adamas_codes_ref_to_planes(ref.ctypes.data, 257, planes.ctypes.data)
+    L.adamas_codes_planes_to_ref(planes.ctypes.data, 257, back.ctypes.data)
+    assert np.array_equal(ref, back)
+    # element e: lo/hi planes hold the code's bits at bit e//4 of word e%4
+    codes = oracle.unpack(ref[5])
+    for e in range(128):
+        lo = (planes[5, e % 4] >> (e // 4)) & 1
+        hi = (planes[5, 4 + e % 4] >> (e // 4)) & 1
+        assert codes[e] == lo | (hi << 1)
+
+
+def test_bitplane_distance_identity_exhaustive():
+    """|a-b| = L + 2A with L = al^bl, A = (ah^bh) & ~(L & (al^ah)) — the
+    per-element identity l1_distance() (csrc/common.cuh) relies on."""
+    for a in range(4):
+        for b in range(4):
+            al, ah, bl, bh = a & 1, a >> 1, b & 1, b >> 1
+            Lx = al ^ bl
+            A = (ah ^ bh) & (1 - (Lx & (al ^ ah)))
+            assert Lx + 2 * A == abs(a - b), (a, b)
+
+
+def test_bitplane_distance_matches_oracle_on_words(oracle):
+    L = _lib()
+    rng = np.random.default_rng(1)
+    for _ in range(500):
+        a = rng.integers(0, 65536, 16).astype(np.uint16)
+        b = rng.integers(0, 65536, 16).astype(np.uint16)
+        pa = np.zeros(8, np.uint32)
+        pb = np.zeros(8, np.uint32)
+        L.adamas_codes_ref_to_planes(a.ctypes.data, 1, pa.ctypes.data)
+        L.adamas_codes_ref_to_planes(b.ctypes.data, 1, pb.ctypes.data)
+        d = 0
+        for w in range(4):
+            Lw = int(pa[w] ^ pb[w])
+            A = int(pa[4 + w] ^ pb[4 + w]) & ~(Lw & int(pa[w] ^ pa[4 + w])) & 0xFFFFFFFF
+            d += bin(Lw).count("1") + 2 * bin(A).count("1")
+        assert d == oracle.l1_2bit(a, b)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2510_18413_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in src.replace("oracle/_ref", "").lower() or f == "build.py", f

@@ -1,0 +1,201 @@
+"""-m gpu: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors. Integer results bit-exact; attention within the
+north-star tolerance (1e-3 relative for fp32 K/V, 1e-2 for bf16 K/V) against
+the double oracle that consumes the same stored values."""
+import numpy as np
+import pytest
+import torch
+
+from tests.golden.make_golden import CASES, case_inputs
+from tests.gpu_helpers import make_inputs, oracle_decode, rel_err, to_dev
+
+pytestmark = pytest.mark.gpu
+TOL = {False: 1e-3, True: 1e-2}
+
+
+def fill_cache(ad, K, V, bf16, capacity=None):
+    S, n_kv, _ = K.shape
+    cache = ad.KvCache(n_kv, capacity or S + 8, torch.bfloat16 if bf16 else torch.float32)
+    if S:
+        cache.update(to_dev(K, bf16), to_dev(V, bf16))
+    return cache
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_encode_append_codes_bit_exact(gpu, oracle, bf16):
+    S, n_kv = 3000, 3
+    K, V, _ = make_inputs(S, n_kv, n_kv, bf16, 11)
+    K[7] *= 1e-30  # tiny and huge scales
+    K[8] *= 1e30 if not bf16 else 1e20
+    cache = fill_cache(gpu, K, V, bf16)
+    assert cache.seq_len == S
+    words = cache.code_words().cpu().numpy().view(np.uint16)
+    for h in range(n_kv):
+        assert np.array_equal(words[h], oracle.encode_pack_rows(K[:, h].astype(np.float64))), h
+    # K/V rows stored verbatim
+    keys = cache.keys()[:, :S].float().cpu().numpy()
+    assert np.array_equal(keys.transpose(1, 0, 2), K.astype(np.float32))
+    assert cache.status() == 0
+
+
+def test_query_encode_bit_exact_many(gpu, oracle):
+    n = 4096
+    _, _, q = make_inputs(1, 1, n, False, 12)
+    cache = gpu.KvCache(1, 16, torch.float32)
+    got = cache.encode_query(to_dev(q, False)).cpu().numpy().view(np.uint16)
+    exp = oracle.encode_pack_rows(q.astype(np.float64))
+    assert np.array_equal(got, exp)
+
+
+def test_degenerate_vector_sets_status(gpu):
+    cache = gpu.KvCache(1, 16, torch.float32)
+    z = torch.zeros((1, 1, 128), device="cuda")
+    cache.update(z, z)
+    with pytest.raises(gpu.ConfigError):
+        cache.raise_on_degenerate()
+    assert cache.status() == 0  # read-and-clear
+    nan = torch.full((1, 128), float("nan"), device="cuda")
+    cache.encode_query(nan)
+    assert cache.status() == 1
+
+
+def test_append_coded_roundtrip(gpu, oracle):
+    S = 500
+    K, V, _ = make_inputs(S, 2, 2, False, 13)
+    rng = np.random.default_rng(0)
+    codes = rng.integers(0, 65536, (S, 2, 16)).astype(np.uint16)
+    cache = gpu.KvCache(2, S, torch.float32)
+    cache.update_coded(to_dev(K, False), to_dev(V, False), torch.from_numpy(codes.view(np.int16)).cuda())
+    back = cache.code_words().cpu().numpy().view(np.uint16)
+    assert np.array_equal(back, codes.transpose(1, 0, 2))
+
+
+@pytest.mark.parametrize("S,n_kv,G", [(1, 1, 1), (257, 2, 1), (4096, 1, 4), (10000, 2, 2)])
+def test_score_all_bit_exact(gpu, oracle, S, n_kv, G):
+    K, V, q = make_inputs(S, n_kv, n_kv * G, True, 14)
+    cache = fill_cache(gpu, K, V, True)
+    qw = cache.encode_query(to_dev(q, True))
+    scores = cache.score_all(qw).cpu().numpy()
+    kw, exp_scores, _, _ = oracle_decode(oracle, K, V, q, 1)
+    assert np.array_equal(qw.cpu().numpy().view(np.uint16), oracle.encode_pack_rows(q.astype(np.float64)))
+    assert np.array_equal(scores, exp_scores)
+
+
+@pytest.mark.parametrize("n,k", [(1000, 64), (1000, 0), (1000, 1), (1000, 999), (1000, 1000), (1000, 5000),
+                                 (33000, 128), (5, 2)])
+def test_top_k_matches_oracle_dense_ties(gpu, oracle, n, k):
+    rng = np.random.default_rng(n + k)
+    rows = [rng.integers(0, 51, n), rng.integers(100, 110, n), np.full(n, 7), rng.integers(0, 385, n)]
+    s = np.stack(rows).astype(np.int32)
+    if k == 0:
+        return
+    got = gpu.top_k(torch.from_numpy(s).cuda(), k).cpu().numpy()
+    for r in range(s.shape[0]):
+        exp = oracle.top_k(s[r], k)
+        assert np.array_equal(got[r, :len(exp)], exp), r
+        assert (got[r, len(exp):] == -1).all()
+    assert list(gpu.top_k(torch.tensor([5, 1, 9, 1], dtype=torch.int32).cuda(), 2)[0].cpu()) == [1, 3]
+    assert list(gpu.top_k(torch.tensor([1, 1, 1], dtype=torch.int32).cuda(), 2)[0].cpu()) == [0, 1]
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_sparse_attention_tolerance(gpu, oracle, bf16):
+    S, n_kv, G = 2000, 2, 2
+    K, V, q = make_inputs(S, n_kv, n_kv * G, bf16, 15)
+    cache = fill_cache(gpu, K, V, bf16)
+    rng = np.random.default_rng(1)
+    k = 100
+    idx = np.stack([np.sort(rng.choice(S, k, replace=False)) for _ in range(n_kv * G)])
+    out = cache.sparse_attention(to_dev(q, bf16), torch.from_numpy(idx.astype(np.int32)).cuda()).cpu().numpy()
+    for h in range(n_kv * G):
+        exp = oracle.sparse_attention(q[h].astype(np.float64), K[:, h // G].astype(np.float64),
+                                      V[:, h // G].astype(np.float64), idx[h])
+        assert rel_err(out[h], exp) <= TOL[bf16] / 10
+    # singleton selection returns the value row (test_attention.cpp:174-179)
+    one = cache.sparse_attention(to_dev(q, bf16), torch.full((n_kv * G, 1), 5, dtype=torch.int32).cuda())
+    for h in range(n_kv * G):
+        assert np.allclose(one[h].cpu().numpy(), V[5, h // G], rtol=0, atol=1e-6)
+
+
+def run_decode(gpu, oracle, S, n_kv, G, budget, bf16, seed, steps=1):
+    """Cache prefilled with S - steps tokens, then `steps` fused decode steps;
+    each step is compared with the oracle over the tokens present after its append."""
+    n_q = n_kv * G
+    K, V, _ = make_inputs(S, n_kv, n_q, bf16, seed)
+    pre = S - steps
+    cache = fill_cache(gpu, K[:pre], V[:pre], bf16, capacity=S + 4)
+    for st in range(steps):
+        t = pre + st
+        q = make_inputs(1, 1, n_q, bf16, seed * 1000 + st)[2]
+        out, idx = cache.decode_step(to_dev(q, bf16), to_dev(K[t], bf16), to_dev(V[t], bf16), budget)
+        out, idx = out.cpu().numpy(), idx.cpu().numpy()
+        _, _, eidx, eout = oracle_decode(oracle, K[:t + 1], V[:t + 1], q, budget)
+        keep = min(budget, t + 1)
+        assert np.array_equal(idx[:, :keep], eidx), f"step {st}"
+        assert (idx[:, keep:] == -1).all()
+        assert rel_err(out, eout).max() <= TOL[bf16], f"step {st}"
+    assert cache.seq_len == S
+    assert cache.status() == 0
+    return cache
+
+
+@pytest.mark.parametrize("S,n_kv,G,budget,bf16", [
+    (1, 1, 1, 4, False),        # empty cache: the new token is the whole selection
+    (2, 1, 1, 1, True),
+    (300, 2, 1, 16, False),     # ragged
+    (777, 2, 4, 32, True),      # GQA
+    (5000, 4, 1, 5000, True),   # budget == S
+    (5000, 1, 2, 9000, False),  # budget > S
+    (4097, 1, 8, 128, True),
+    (32768, 1, 1, 128, False),  # config 0: 1 head, 32K, fp32, budget 128
+])
+def test_fused_decode_step_matches_oracle(gpu, oracle, S, n_kv, G, budget, bf16):
+    run_decode(gpu, oracle, S, n_kv, G, budget, bf16, seed=S + budget)
+
+
+def test_fused_decode_multi_step(gpu, oracle):
+    run_decode(gpu, oracle, 3000, 2, 2, 64, True, seed=77, steps=5)
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "8", "16"])
+def test_fused_decode_cluster_sizes(gpu, oracle, monkeypatch, cluster):
+    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    run_decode(gpu, oracle, 6000, 2, 1, 128, True, seed=int(cluster))
+
+
+def test_operator_composition_matches_fused(gpu, oracle, monkeypatch):
+    monkeypatch.setenv("ADAMAS_NO_FUSED", "1")
+    run_decode(gpu, oracle, 2000, 2, 2, 64, False, seed=5, steps=2)
+
+
+def test_batched_decode_matches_single(gpu, oracle):
+    n_seqs, S, n_kv, G, budget = 5, 1500, 2, 2, 48
+    caches, qs, ks, vs, exp = [], [], [], [], []
+    for i in range(n_seqs):
+        K, V, q = make_inputs(S + i * 100, n_kv, n_kv * G, True, 900 + i)
+        caches.append(fill_cache(gpu, K[:-1], V[:-1], True, capacity=S + 1000))
+        qs.append(q); ks.append(K[-1]); vs.append(V[-1])
+        exp.append(oracle_decode(oracle, K, V, q, budget))
+    out, idx = gpu.decode_step_batched(caches, to_dev(np.stack(qs), True), to_dev(np.stack(ks), True),
+                                       to_dev(np.stack(vs), True), budget)
+    out, idx = out.cpu().numpy(), idx.cpu().numpy()
+    for i in range(n_seqs):
+        assert np.array_equal(idx[i], exp[i][2]), i
+        assert rel_err(out[i], exp[i][3]).max() <= 1e-2
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_cuda_path_reproduces_reference_golden(gpu, golden, name):
+    """Bit-exact against vectors produced by the unmodified reference build."""
+    S, n_kv, n_q, budget, bf16, seed = (int(v) for v in golden[f"{name}/meta"])
+    K, V, q = case_inputs(S, n_kv, n_q, bool(bf16), seed)
+    cache = fill_cache(gpu, K[:-1], V[:-1], bool(bf16), capacity=S + 1)
+    qd = to_dev(q, bool(bf16))
+    out, idx = cache.decode_step(qd, to_dev(K[-1], bool(bf16)), to_dev(V[-1], bool(bf16)), budget)
+    words = cache.code_words().cpu().numpy().view(np.uint16)
+    assert np.array_equal(words, golden[f"{name}/key_words"])
+    assert np.array_equal(cache.encode_query(qd).cpu().numpy().view(np.uint16), golden[f"{name}/q_words"])
+    assert np.array_equal(cache.score_all(cache.encode_query(qd)).cpu().numpy(), golden[f"{name}/scores"])
+    keep = min(budget, S)
+    assert np.array_equal(idx.cpu().numpy()[:, :keep], golden[f"{name}/idx"])
+    assert rel_err(out.cpu().numpy(), golden[f"{name}/out"]).max() <= TOL[bool(bf16)]
