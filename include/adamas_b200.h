@@ -138,6 +138,11 @@ int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const vo
                                const void* k_new, const void* v_new, int64_t budget, float* out,
                                int32_t* idx, void* stream);
 
+/* ---------------------------------------------------------------- diagnostics
+ * Subsequent fused decode launches write up to 16 %globaltimer stamps per CTA
+ * (phase boundaries) into device_buffer[blockIdx * 16 + i]; NULL disables. */
+void adamas_debug_trace(unsigned long long* device_buffer);
+
 /* ---------------------------------------------------------------- host converters */
 
 /* Reference PackedCodes words <-> device bit-plane record (32 B), host memory,

@@ -23,7 +23,7 @@ EXPORTED = [
     "adamas_cache_append", "adamas_cache_append_coded", "adamas_cache_codes_ref",
     "adamas_encode_query", "adamas_score", "adamas_topk", "adamas_sparse_attention",
     "adamas_decode_step", "adamas_decode_step_batched", "adamas_codes_ref_to_planes",
-    "adamas_codes_planes_to_ref",
+    "adamas_codes_planes_to_ref", "adamas_debug_trace",
 ]
 
 
@@ -65,6 +65,7 @@ def load() -> C.CDLL:
     L.adamas_decode_step_batched.argtypes = [C.POINTER(vp), i32, vp, i32, vp, vp, i64, vp, vp, vp]
     L.adamas_codes_ref_to_planes.argtypes = [vp, i64, vp]
     L.adamas_codes_planes_to_ref.argtypes = [vp, i64, vp]
+    L.adamas_debug_trace.argtypes = [vp]
     for name in EXPORTED:
         if not hasattr(L, name):
             raise ImportError(f"{LIB} does not export {name}")

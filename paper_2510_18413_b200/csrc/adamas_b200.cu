@@ -34,6 +34,7 @@ struct adamas_cache {
 namespace {
 
 thread_local std::string g_last_error;
+unsigned long long* g_trace = nullptr;  // adamas_debug_trace
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -183,25 +184,41 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
     C = 1;
     while (C < 16 && units * C * 2 <= sm_count()) C *= 2;
   }
-  const size_t smem_cap = 200 * 1024;
   for (;;) {
     int64_t chunk = (s_max + C - 1) / C;
     chunk = (chunk + 255) / 256 * 256;
     const int selcap = (int)std::min<int64_t>(budget, chunk);
-    const FusedSmem L(G, C, (int)chunk, selcap);
-    if (L.total <= smem_cap) {
+    // one CTA per SM when the grid fits the machine, else two
+    const size_t smem_cap = (size_t)units * C <= (size_t)sm_count() ? 215 * 1024 : 108 * 1024;
+    const FusedSmem base(G, C, (int)chunk, selcap, 0);
+    const int want = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (chunk + kStageTok - 1) / kStageTok));
+    int stages = env_int("ADAMAS_STAGES", 0);
+    if (stages <= 0) {
+      stages = want;
+      while (stages > 2 && base.total + (size_t)stages * kStageTok * 32 > smem_cap) --stages;
+    }
+    const FusedSmem L(G, C, (int)chunk, selcap, stages);
+    if (chunk > 65280) {  // u16 histogram exchange: per-rank counts must stay < 2^16
+      if (C >= 16) return kFusedUnsupported;
+      C *= 2;
+      continue;
+    }
+    if (L.total <= smem_cap || (stages == 2 && L.total <= 215 * 1024)) {
       FusedParams prm{};
       prm.n_seqs = n_seqs;
       prm.n_kv = n_kv;
       prm.C = C;
       prm.chunk = (int)chunk;
       prm.budget = (int)budget;
+      prm.stages = stages;
+      prm.exact_encode = env_int("ADAMAS_EXACT_ENCODE", 0);
       prm.q = q;
       prm.k_new = k_new;
       prm.v_new = v_new;
       prm.out = out;
       prm.idx = idx;
       prm.status = caches[0]->status;
+      prm.trace = g_trace;
       for (int i = 0; i < n_seqs; ++i) {
         prm.seq[i].codes = caches[i]->codes;
         prm.seq[i].K = caches[i]->K;
@@ -220,6 +237,8 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
 }  // namespace
 
 extern "C" {
+
+void adamas_debug_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
 
 const char* adamas_version(void) { return "adamas-b200 0.1 (sm_100a)"; }
 

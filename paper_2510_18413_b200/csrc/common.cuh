@@ -108,9 +108,11 @@ struct Elem<__nv_bfloat16> {
 // All arithmetic is fp64 with explicit _rn intrinsics (no FMA contraction),
 // the butterflies in the reference's stage order and the sum of squares in
 // index order, so the codes are bit-identical to the reference's.
-// `sq` is a 128-double per-warp scratch in shared memory.
+// `sq` is a 128-double per-warp scratch in shared memory. fast = true takes a
+// provably equivalent low-latency route for sigma (see below) with the exact
+// sequential sum as its fallback.
 // Returns false (and zero codes) for a zero / non-finite vector.
-__device__ __forceinline__ bool encode128_warp(const float in[4], double* sq, Code& out) {
+__device__ __forceinline__ bool encode128_warp(const float in[4], double* sq, Code& out, bool fast = false) {
   const int lane = threadIdx.x & 31;
   double x[4];
 #pragma unroll
@@ -143,15 +145,40 @@ __device__ __forceinline__ bool encode128_warp(const float in[4], double* sq, Co
                    : __dmul_rn(__dadd_rn(x[j], p), kInvSqrt2);
     }
   }
-  // sum of squares in index order 0..127 (quantizer.cpp:43-44)
+  double sq4[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) sq[lane * 4 + j] = __dmul_rn(x[j], x[j]);
-  __syncwarp();
-  double sumsq = 0.0;
+  for (int j = 0; j < 4; ++j) sq4[j] = __dmul_rn(x[j], x[j]);
+  double sigma;
+  bool exact = !fast;
+  if (fast) {
+    // Latency path: a shuffle-tree sum of the same 128 exact products. Any
+    // two summation orders of n = 128 non-negative terms agree to within
+    // 2 (n-1) u ~= 2.9e-14 relative, so sigma and the +/-kQ28 sigma thresholds
+    // to within ~2e-14 relative. Codes can only differ for an element within
+    // that distance of a threshold (the 0 threshold does not depend on sigma);
+    // if any element is within 1e-12 of one, or the sum is near the fp64
+    // range ends where relative bounds fail, take the exact sequential path.
+    double s4 = __dadd_rn(__dadd_rn(sq4[0], sq4[1]), __dadd_rn(sq4[2], sq4[3]));
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) s4 = __dadd_rn(s4, __shfl_xor_sync(kFull, s4, m));
+    sigma = __dsqrt_rn(__ddiv_rn(s4, (double)kHeadDim));
+    const double t = __dmul_rn(kQ28, sigma);
+    bool near = !(s4 > 1e-290 && s4 < 1e300);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) near |= fabs(fabs(x[j]) - t) <= 1e-12 * t;
+    exact = __any_sync(kFull, near);
+  }
+  if (exact) {
+    // sum of squares in index order 0..127 (quantizer.cpp:43-44)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sq[lane * 4 + j] = sq4[j];
+    __syncwarp();
+    double sumsq = 0.0;
 #pragma unroll 16
-  for (int e = 0; e < kHeadDim; ++e) sumsq = __dadd_rn(sumsq, sq[e]);
-  __syncwarp();
-  const double sigma = __dsqrt_rn(__ddiv_rn(sumsq, (double)kHeadDim));
+    for (int e = 0; e < kHeadDim; ++e) sumsq = __dadd_rn(sumsq, sq[e]);
+    __syncwarp();
+    sigma = __dsqrt_rn(__ddiv_rn(sumsq, (double)kHeadDim));
+  }
   const bool ok = isfinite(sigma) && sigma != 0.0;
   const double t_hi = __dmul_rn(kQ28, sigma);
   const double t_lo = __dmul_rn(-kQ28, sigma);
@@ -197,6 +224,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Cluster / DSMEM primitives. Remote shared-memory traffic uses st.async with
+// mbarrier transaction counting on the receiving CTA, so no cluster-wide
+// barrier (and no GPU-scope fence) sits on the data path.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t remote_bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          remote_addr),
+      "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// Bulk L2 prefetch (TMA engine): warms `bytes` (multiple of 16) of global memory.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

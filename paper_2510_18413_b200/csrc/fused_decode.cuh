@@ -5,37 +5,38 @@
 // token range [r * chunk, min(S, (r + 1) * chunk)) where S includes the token
 // appended by this very step (Alg. 1: update before estimate).
 //
-//   prologue  warps 0..G-1 encode the G query heads (fp64 FWHT + RMS
-//             thresholds, bit-exact); the rank owning position S-1 encodes the
-//             new key and appends (k, v, code) to the cache (kv_cache.cpp:62-71)
-//   scan      bulk-copy (TMA engine) ring streams the range's lo/hi code planes
-//             HBM -> smem; every token's G distances (estimator.cpp:45-59) go
-//             to a u16 smem array and a per-CTA 512-bin smem histogram
-//   select    cluster barrier; every rank reads all C histograms over DSMEM and
-//             derives the global threshold T (k-th smallest), how many ties at
-//             T the ranks before it take, and its output offset; then an
-//             order-preserving warp-ballot compaction of its own tokens
-//             (top_k semantics, estimator.cpp:75-90: (score, index) order)
+//   prologue  one lane starts the bulk-copy (TMA engine) stream of the rank's
+//             lo/hi code planes into a deep shared-memory ring; warps 0..G-1
+//             encode the G query heads (fp64 FWHT + RMS thresholds, bit-exact)
+//             meanwhile; the rank owning position S-1 encodes the new key and
+//             appends (k, v, code) to the cache (kv_cache.cpp:62-71)
+//   scan      each thread turns two tokens per stage into G exact distances
+//             (estimator.cpp:45-59), kept as u16 in shared memory and counted
+//             in a per-CTA 512-bin histogram per q-head
+//   select    cluster barrier; every rank reads the C histograms over DSMEM,
+//             derives the global threshold T (k-th smallest distance), how many
+//             ties at T earlier ranks take and its own output offset; then an
+//             order-preserving warp compaction of its own tokens (top_k
+//             semantics, estimator.cpp:75-90: (score, index) order)
 //   attend    each rank attends over its own selected rows (gather of K, V by
-//             index, fp32 online softmax) and pushes (m, l, o[128]) into the
-//             merging rank's smem over DSMEM; cluster barrier; log-sum-exp
-//             merge -> out (attention.cpp:8-45 semantics)
+//             index, fp32 online softmax), pushes (m, l, o[128]) into the
+//             merging rank's shared memory over DSMEM; cluster barrier;
+//             log-sum-exp merge -> out (attention.cpp:8-45 semantics)
 //
 // Indices are bit-exact by construction: the selection is computed from the
 // exact integer distances with the reference's total order, no approximation.
 #pragma once
-#include <cooperative_groups.h>
-
 #include "ops.cuh"
 
 namespace adamas_dev {
-namespace cg = cooperative_groups;
 
-constexpr int kFusedThreads = 256;
+constexpr int kFusedThreads = 512;
 constexpr int kFusedWarps = kFusedThreads / 32;
-constexpr int kStageTok = 512;  // tokens per bulk-copy stage: 2 x 8 KB planes
-constexpr int kStages = 4;
-constexpr int kHistBins = 512;  // 2-bit L1 distances at d = 128 are <= 384
+constexpr int kStageTok = 1024;  // tokens per bulk-copy stage: 2 x 16 KB planes
+constexpr int kStageBytes = kStageTok * 32;
+constexpr int kMaxStages = 16;   // ring depth cap (runtime: FusedParams::stages)
+constexpr int kHistBins = 512;   // 2-bit L1 distances at d = 128 are <= 384
+constexpr int kMaxG = 8;
 constexpr int kMaxSeqs = 64;
 constexpr int kPartStride = 132;  // floats per partial: m, l, pad, pad, o[128]
 constexpr int kFusedUnsupported = -100;
@@ -49,64 +50,91 @@ struct FusedSeq {
 };
 
 struct FusedParams {
-  int n_seqs, n_kv, C, chunk, budget;
+  int n_seqs, n_kv, C, chunk, budget, stages;
+  int exact_encode;  // 1: always the sequential fp64 sum (diagnostics / tests)
   const void* q;      // [n_seqs][n_q][128]
   const void* k_new;  // [n_seqs][n_kv][128]
   const void* v_new;
   float* out;    // [n_seqs][n_q][128]
   int32_t* idx;  // [n_seqs][n_q][budget] or null
   int* status;
+  unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
   FusedSeq seq[kMaxSeqs];
 };
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ADAMAS_TRACE(i) \
+  do { if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (i)] = global_ns(); } while (0)
+
 // Dynamic shared-memory carve-up, identical on host and device.
 struct FusedSmem {
-  uint32_t stage, dist, hist, sel, inbox, wpart, qcode, sq, bars, scal, total;
-  __host__ __device__ static uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
-  __host__ __device__ FusedSmem(int G, int C, int chunk, int selcap) {
+  uint32_t stage, dist, hist, hist_all, sel, inbox, wpart, qcode, sq, bars, total;
+  __host__ __device__ static uint32_t align(uint32_t x, uint32_t a) { return (x + a - 1u) & ~(a - 1u); }
+  __host__ __device__ FusedSmem(int G, int C, int chunk, int selcap, int stages) {
     uint32_t o = 0;
-    stage = o; o += kStages * kStageTok * 32;
-    dist = o;  o = align16(o + (uint32_t)G * chunk * 2);
+    stage = o; o += (uint32_t)stages * kStageBytes;
+    dist = o;  o = align(o + (uint32_t)G * chunk * 2, 16);
     hist = o;  o += (uint32_t)G * kHistBins * 4;
-    sel = o;   o = align16(o + (uint32_t)G * selcap * 4);
+    hist_all = o; o += (uint32_t)C * G * kHistBins * 2;  // u16 histograms received from every rank
+    sel = o;   o = align(o + (uint32_t)G * selcap * 4, 16);
     inbox = o; o += (uint32_t)C * G * kPartStride * 4;
     wpart = o; o += kFusedWarps * kPartStride * 4;
-    o = (o + 31u) & ~31u;
+    o = align(o, 32);
     qcode = o; o += (uint32_t)(G + 1) * 32;
-    sq = o;    o += kFusedWarps * kHeadDim * 8;
-    bars = o;  o += kStages * 8;
-    scal = o;  o += 64 * 4;
+    sq = o;    o += (uint32_t)(G + 1) * kHeadDim * 8;
+    bars = o;  o += (kMaxStages + 2) * 8;  // ring, hist exchange, partial exchange
     total = o;
   }
 };
 
-// Exclusive scan over the CTA of up to three ints (thread order).
-__device__ __forceinline__ void block_scan3(int a, int b, int c, int* scratch /*3*32*/, int& ea, int& eb,
-                                            int& ec) {
+// Exclusive CTA-wide scan (thread order) of N ints per thread.
+template <int N>
+__device__ __forceinline__ void block_scan(int (&v)[N], int (&excl)[N], int (&total)[N], int* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int ia = a, ib = b, ic = c;
+  int incl[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) incl[i] = v[i];
 #pragma unroll
   for (int m = 1; m < 32; m <<= 1) {
-    const int ta = __shfl_up_sync(kFull, ia, m), tb = __shfl_up_sync(kFull, ib, m),
-              tc = __shfl_up_sync(kFull, ic, m);
-    if (lane >= m) { ia += ta; ib += tb; ic += tc; }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int o = __shfl_up_sync(kFull, incl[i], m);
+      if (lane >= m) incl[i] += o;
+    }
   }
-  if (lane == 31) { scratch[warp] = ia; scratch[32 + warp] = ib; scratch[64 + warp] = ic; }
+  if (lane == 31) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) scratch[i * kFusedWarps + warp] = incl[i];
+  }
   __syncthreads();
-  int wa = 0, wb = 0, wc = 0;
-  for (int w = 0; w < warp; ++w) { wa += scratch[w]; wb += scratch[32 + w]; wc += scratch[64 + w]; }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    int before = 0, sum = 0;
+    for (int w = 0; w < kFusedWarps; ++w) {
+      const int x = scratch[i * kFusedWarps + w];
+      before += w < warp ? x : 0;
+      sum += x;
+    }
+    excl[i] = before + incl[i] - v[i];
+    total[i] = sum;
+  }
   __syncthreads();
-  ea = wa + ia - a;
-  eb = wb + ib - b;
-  ec = wc + ic - c;
 }
 
 template <typename T, int G>
 __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+  static_assert(G >= 1 && G <= kMaxG && (kFusedWarps % G) == 0, "G must divide the warp count");
   extern __shared__ __align__(128) uint8_t smem[];
-  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ int scan_scratch[2 * kMaxG * kFusedWarps];
+  __shared__ int sc[kMaxG][4];  // per q-head: T, below, pre_lt, pre_eq
+  __shared__ int warp_cnt[kFusedWarps][2];
+  __shared__ int nsel[kMaxG];
   const int C = p.C;
-  const int rank = (int)cluster.block_rank();
+  const int rank = (int)cluster_rank();
   const int unit = blockIdx.x / C;
   const int si = unit / p.n_kv, hk = unit % p.n_kv;
   const int n_q = p.n_kv * G;
@@ -121,51 +149,65 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
   const int mem_len = (int)max((int64_t)0, min(end, s_old) - start);  // already in HBM
   const bool has_new = (s_old >= start) && (s_old < end);
   const int selcap = min(p.budget, p.chunk);
+  const int ring = p.stages;
 
-  const FusedSmem L(G, C, p.chunk, selcap);
+  const FusedSmem L(G, C, p.chunk, selcap, ring);
   uint4* stage = reinterpret_cast<uint4*>(smem + L.stage);
   uint16_t* dist = reinterpret_cast<uint16_t*>(smem + L.dist);
   int* hist = reinterpret_cast<int*>(smem + L.hist);
+  uint16_t* hist_all = reinterpret_cast<uint16_t*>(smem + L.hist_all);
   int* sel = reinterpret_cast<int*>(smem + L.sel);
   float* inbox = reinterpret_cast<float*>(smem + L.inbox);
   float* wpart = reinterpret_cast<float*>(smem + L.wpart);
   Code* qcode = reinterpret_cast<Code*>(smem + L.qcode);
   double* sqs = reinterpret_cast<double*>(smem + L.sq);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  int* scal = reinterpret_cast<int*>(smem + L.scal);
+  uint64_t* hist_bar = bars + kMaxStages;
+  uint64_t* inbox_bar = bars + kMaxStages + 1;
+  int n_owned = 0;  // q-heads whose final merge this rank performs
+  for (int g = rank; g < G; g += C) ++n_owned;
 
   uint4* planes = p.seq[si].codes + (int64_t)hk * 2 * cap;  // lo plane; hi = +cap
   const uint4* lo_g = planes + start;
   const uint4* hi_g = planes + cap + start;
 
   // ---------------------------------------------------------------- prologue
-  for (int i = tid; i < G * kHistBins; i += kFusedThreads) hist[i] = 0;
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
+  ADAMAS_TRACE(0);
   const int n_stages = (mem_len + kStageTok - 1) / kStageTok;
+  constexpr int kIssueWarp = kFusedWarps - 1;
   auto issue = [&](int st) {
-    const int slot = st % kStages;
+    const int slot = st % ring;
     const int ntok = min(kStageTok, mem_len - st * kStageTok);
     const uint32_t bytes = (uint32_t)ntok * 16u;
+    uint4* dst = stage + (size_t)slot * (kStageBytes / 16);
     mbar_expect_tx(&bars[slot], 2u * bytes);
-    bulk_g2s(stage + slot * 2 * kStageTok, lo_g + (int64_t)st * kStageTok, bytes, &bars[slot]);
-    bulk_g2s(stage + slot * 2 * kStageTok + kStageTok, hi_g + (int64_t)st * kStageTok, bytes, &bars[slot]);
+    bulk_g2s(dst, lo_g + (int64_t)st * kStageTok, bytes, &bars[slot]);
+    bulk_g2s(dst + kStageTok, hi_g + (int64_t)st * kStageTok, bytes, &bars[slot]);
   };
-  if (tid == 0)
-    for (int st = 0; st < min(kStages, n_stages); ++st) issue(st);
+  if (warp == kIssueWarp && lane == 0) {  // the code stream starts before anything else
+    for (int s = 0; s < ring; ++s) mbar_init(&bars[s], 1);
+    mbar_init(hist_bar, 1);
+    mbar_init(inbox_bar, 1);
+    mbar_fence_init();
+    for (int st = 0; st < min(ring, n_stages); ++st) issue(st);
+    // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
+    // C partials per q-head it merges
+    mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
+    if (n_owned) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
+  }
+  for (int i = tid; i < G * kHistBins; i += kFusedThreads) hist[i] = 0;
+  ADAMAS_TRACE(1);
 
   if (warp < G) {  // encode query head hk * G + warp (sweep.cpp:92-94)
     const T* qp = reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + (int64_t)hk * G + warp) * kHeadDim;
     float f[4];
     Raw4<T>::to_float(Raw4<T>::load(qp + lane * 4), f);
     Code c;
-    if (!encode128_warp(f, sqs + warp * kHeadDim, c) && lane == 0) atomicOr(p.status, kStatusDegenerate);
+    if (!encode128_warp(f, sqs + warp * kHeadDim, c, !p.exact_encode) && lane == 0)
+      atomicOr(p.status, kStatusDegenerate);
     if (lane == 0) qcode[warp] = c;
   }
-  if (has_new && warp == (G % kFusedWarps)) {  // append (kv_cache.cpp:62-71)
+  if (has_new && warp == G) {  // append (kv_cache.cpp:62-71)
     const int64_t vrow = (int64_t)si * p.n_kv + hk;
     const T* kp = reinterpret_cast<const T*>(p.k_new) + vrow * kHeadDim;
     const T* vp = reinterpret_cast<const T*>(p.v_new) + vrow * kHeadDim;
@@ -177,37 +219,49 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     float f[4];
     Raw4<T>::to_float(kr, f);
     Code c;
-    if (!encode128_warp(f, sqs + warp * kHeadDim, c) && lane == 0) atomicOr(p.status, kStatusDegenerate);
+    if (!encode128_warp(f, sqs + G * kHeadDim, c, !p.exact_encode) && lane == 0)
+      atomicOr(p.status, kStatusDegenerate);
     if (lane == 0) {
       qcode[G] = c;
       store_code(planes, cap, s_old, c);
     }
   }
   __syncthreads();
+  cluster_arrive_relaxed();  // "my mbarriers are initialized"; waited on before the first DSMEM store
   QCode qc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) qc[g] = make_qcode(qcode[g]);
 
   // ---------------------------------------------------------------- scan
+  ADAMAS_TRACE(2);
   for (int st = 0; st < n_stages; ++st) {
-    const int slot = st % kStages;
-    mbar_wait(&bars[slot], (uint32_t)(st / kStages) & 1u);
-    const uint4* slo = stage + slot * 2 * kStageTok;
+    const int slot = st % ring;
+    mbar_wait(&bars[slot], (uint32_t)(st / ring) & 1u);
+    const uint4* slo = stage + (size_t)slot * (kStageBytes / 16);
     const uint4* shi = slo + kStageTok;
     const int base = st * kStageTok;
     const int ntok = min(kStageTok, mem_len - base);
-    for (int j = tid; j < ntok; j += kFusedThreads) {
-      const uint4 a = slo[j], b = shi[j];
-      const uint32_t lo[4] = {a.x, a.y, a.z, a.w}, hi[4] = {b.x, b.y, b.z, b.w};
+    uint4 a[2], b[2];
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const uint32_t d = l1_distance(qc[g], lo, hi);
-        dist[g * p.chunk + base + j] = (uint16_t)d;
-        atomicAdd(&hist[g * kHistBins + d], 1);
+    for (int u = 0; u < 2; ++u) {
+      const int j = tid + u * kFusedThreads;
+      if (j < ntok) { a[u] = slo[j]; b[u] = shi[j]; }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = tid + u * kFusedThreads;
+      if (j < ntok) {
+        const uint32_t lo[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, hi[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t d = l1_distance(qc[g], lo, hi);
+          dist[g * p.chunk + base + j] = (uint16_t)d;
+          atomicAdd(&hist[g * kHistBins + d], 1);
+        }
       }
     }
     __syncthreads();
-    if (tid == 0 && st + kStages < n_stages) issue(st + kStages);
+    if (warp == kIssueWarp && lane == 0 && st + ring < n_stages) issue(st + ring);
   }
   if (has_new && tid < G) {  // the appended token is a candidate
     const Code nc = qcode[G];
@@ -215,107 +269,160 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     dist[tid * p.chunk + (int)(s_old - start)] = (uint16_t)d;
     atomicAdd(&hist[tid * kHistBins + d], 1);
   }
-  cluster.sync();  // #1: every rank's histogram is final
+  ADAMAS_TRACE(3);
+  __syncthreads();  // local histogram final
+  // Push this rank's histograms (as u16, counts <= chunk < 2^16) into every
+  // rank's hist_all[rank] with st.async; each receiver's mbarrier counts bytes.
+  cluster_wait();
+  if (tid < G * (kHistBins / 8)) {
+    const int g = tid / (kHistBins / 8), b0 = (tid % (kHistBins / 8)) * 8;
+    const int4 h0 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0);
+    const int4 h1 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0 + 4);
+    const uint32_t w0 = (uint32_t)h0.x | ((uint32_t)h0.y << 16), w1 = (uint32_t)h0.z | ((uint32_t)h0.w << 16);
+    const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)h1.w << 16);
+    const uint32_t local = smem_addr(hist_all + ((size_t)rank * G + g) * kHistBins + b0);
+    for (int r = 0; r < C; ++r)
+      st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), r));
+  }
+  mbar_wait(hist_bar, 0);
+  ADAMAS_TRACE(4);
 
-  // ---------------------------------------------------------------- select
+  // ---------------------------------------------------------------- threshold
+  // thread t owns distance bin t of every q-head
   const int k_eff = (int)min((int64_t)p.budget, S);
-  int* sc = scal;  // per g: [0] T, [1] below, [2] pre_lt, [3] pre_eq, [4] own_lt, [5] own_eq
-  __shared__ int scan_scratch[96];
-  __shared__ int row_tot[2];
-#pragma unroll 1
-  for (int g = 0; g < G; ++g) {
-    const int b0 = 2 * tid, b1 = 2 * tid + 1;
-    int tot0 = 0, tot1 = 0, pre0 = 0, pre1 = 0;
+  {
+    int tot[G], pre[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { tot[g] = 0; pre[g] = 0; }
     for (int r = 0; r < C; ++r) {
-      const int* rh = cluster.map_shared_rank(hist, r) + g * kHistBins;
-      const int2 h = *reinterpret_cast<const int2*>(rh + b0);
-      tot0 += h.x;
-      tot1 += h.y;
-      if (r < rank) { pre0 += h.x; pre1 += h.y; }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int h = hist_all[((size_t)r * G + g) * kHistBins + tid];
+        tot[g] += h;
+        pre[g] += r < rank ? h : 0;
+      }
     }
-    const int own0 = hist[g * kHistBins + b0], own1 = hist[g * kHistBins + b1];
-    int etot, epre, eown;
-    block_scan3(tot0 + tot1, pre0 + pre1, own0 + own1, scan_scratch, etot, epre, eown);
-    if (etot < k_eff && etot + tot0 >= k_eff) {
-      sc[g * 6 + 0] = b0; sc[g * 6 + 1] = etot; sc[g * 6 + 2] = epre; sc[g * 6 + 3] = pre0;
-      sc[g * 6 + 4] = eown; sc[g * 6 + 5] = own0;
-    } else if (etot + tot0 < k_eff && etot + tot0 + tot1 >= k_eff) {
-      sc[g * 6 + 0] = b1; sc[g * 6 + 1] = etot + tot0; sc[g * 6 + 2] = epre + pre0; sc[g * 6 + 3] = pre1;
-      sc[g * 6 + 4] = eown + own0; sc[g * 6 + 5] = own1;
+    ADAMAS_TRACE(5);
+    int v[2 * G], ex[2 * G], sum[2 * G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { v[g] = tot[g]; v[G + g] = pre[g]; }
+    block_scan<2 * G>(v, ex, sum, scan_scratch);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (ex[g] < k_eff && ex[g] + tot[g] >= k_eff) {  // this bin holds the k-th smallest
+        sc[g][0] = tid;        // T
+        sc[g][1] = ex[g];      // count of distances < T over the whole head
+        sc[g][2] = ex[G + g];  // count of distances < T in ranks before this one
+        sc[g][3] = pre[g];     // count of distances == T in ranks before this one
+      }
     }
   }
   __syncthreads();
+  ADAMAS_TRACE(6);
 
-  // order-preserving compaction: warp w walks 256-token slabs of its range
-  const int n_slab = (len + 255) / 256;
-#pragma unroll 1
-  for (int g = 0; g < G; ++g) {
-    const int thr = sc[g * 6 + 0], below = sc[g * 6 + 1], pre_lt = sc[g * 6 + 2], pre_eq = sc[g * 6 + 3];
-    const int need = k_eff - below;                     // ties at T the whole head takes
-    const int eq_budget = max(0, need - pre_eq);        // ... of which this rank may take
-    const int out_off = pre_lt + min(pre_eq, need);     // selected tokens in earlier ranks
+  // ---------------------------------------------------------------- compaction
+  // Warp w serves q-head g = w % G over sub-range w / G of this rank's tokens;
+  // lane l reads 8 consecutive distances per 256-token step, so the
+  // (sub-range, step, lane) order is index order. Pass 1 counts (< T, == T)
+  // per warp; pass 2 re-walks with a packed warp scan and emits in order.
+  {
+    constexpr int WG = kFusedWarps / G;
+    const int g = warp % G, sub = warp / G;
+    const int per_warp = ((len + WG - 1) / WG + 255) / 256 * 256;
+    const int wbeg = sub * per_warp, wend = min(len, wbeg + per_warp);
+    const int thr = sc[g][0], below = sc[g][1], pre_lt = sc[g][2], pre_eq = sc[g][3];
+    const int need = k_eff - below;               // ties at T the whole head takes
+    const int eq_budget = max(0, need - pre_eq);  // ... of which this rank may take
+    const int out_off = pre_lt + min(pre_eq, need);
     const uint16_t* dg = dist + g * p.chunk;
-    // rows of kFusedWarps slabs in index order; thread order == token order
-    int run_lt = 0, run_eq = 0;  // CTA-wide counts before the current slab row
-    for (int row0 = 0; row0 < n_slab; row0 += kFusedWarps) {
-      const int sl = row0 + warp;
-      const int t0 = sl * 256 + lane * 8;
-      int lt = 0, eq = 0;
-      uint32_t ltm = 0, eqm = 0;
-      if (sl < n_slab && t0 < len) {
-        const uint4 v = *reinterpret_cast<const uint4*>(dg + t0);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    auto masks = [&](int t0, uint32_t& ltm, uint32_t& eqm) {
+      ltm = 0;
+      eqm = 0;
+      if (t0 < wend) {
+        const uint4 vv = *reinterpret_cast<const uint4*>(dg + t0);
+        const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int d = (int)((w[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-          const bool valid = t0 + e < len;
-          if (valid && d < thr) ltm |= 1u << e;
-          if (valid && d == thr) eqm |= 1u << e;
-        }
-        lt = __popc(ltm);
-        eq = __popc(eqm);
-      }
-      int elt, eeq, dummy;
-      block_scan3(lt, eq, 0, scan_scratch, elt, eeq, dummy);
-      // CTA-wide exclusive counts for this lane's 8 tokens
-      const int lt_before = run_lt + elt, eq_before = run_eq + eeq;
-      int pos = lt_before + min(eq_before, eq_budget);
-      int eq_seen = eq_before;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        bool take = (ltm >> e) & 1u;
-        if ((eqm >> e) & 1u) {
-          take = eq_seen < eq_budget;
-          ++eq_seen;
-        }
-        if (take) {
-          const int tok = (int)start + t0 + e;
-          if (pos < selcap) sel[g * selcap + pos] = tok;
-          if (p.idx) p.idx[((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off + pos] = tok;
-          ++pos;
+          const bool valid = t0 + e < wend;
+          ltm |= (uint32_t)(valid && d < thr) << e;
+          eqm |= (uint32_t)(valid && d == thr) << e;
         }
       }
-      // totals of this row of slabs
-      if (tid == kFusedThreads - 1) { row_tot[0] = elt + lt; row_tot[1] = eeq + eq; }
-      __syncthreads();
-      run_lt += row_tot[0];
-      run_eq += row_tot[1];
-      __syncthreads();
+    };
+    const T* Kg = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
+    const T* Vg = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
+    unsigned cnt = 0;  // packed: lt in bits 0..15, eq in bits 16..31
+    for (int t0 = wbeg + lane * 8; t0 - lane * 8 < wend; t0 += 256) {
+      uint32_t ltm, eqm;
+      masks(t0, ltm, eqm);
+      cnt += (unsigned)__popc(ltm) | ((unsigned)__popc(eqm) << 16);
+      // candidates (d <= T): start pulling their K and V rows into L2 now, so
+      // the gather after the compaction hits L2 instead of HBM
+      for (uint32_t m = ltm | eqm; m; m &= m - 1) {
+        const int t = t0 + __ffs(m) - 1;
+        prefetch_l2_bulk(Kg + (int64_t)t * kHeadDim, kHeadDim * sizeof(T));
+        prefetch_l2_bulk(Vg + (int64_t)t * kHeadDim, kHeadDim * sizeof(T));
+      }
     }
-    if (tid == 0) scal[48 + g] = min(run_lt + min(run_eq, eq_budget), selcap);  // rows this rank attends
-  }
-  if (rank == 0 && p.idx) {  // estimator.cpp:80 caps the selection at S
-    for (int g = 0; g < G; ++g)
-      for (int i = k_eff + tid; i < p.budget; i += kFusedThreads)
-        p.idx[((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + i] = -1;
+    cnt = __reduce_add_sync(kFull, cnt);
+    if (lane == 0) { warp_cnt[warp][0] = (int)(cnt & 0xffffu); warp_cnt[warp][1] = (int)(cnt >> 16); }
+    __syncthreads();
+    ADAMAS_TRACE(7);
+    int run_lt = 0, run_eq = 0, tot_lt = 0, tot_eq = 0;
+    for (int s2 = 0; s2 < WG; ++s2) {
+      const int w2 = s2 * G + g;
+      if (s2 < sub) { run_lt += warp_cnt[w2][0]; run_eq += warp_cnt[w2][1]; }
+      tot_lt += warp_cnt[w2][0];
+      tot_eq += warp_cnt[w2][1];
+    }
+    int32_t* idx_row = p.idx ? p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off : nullptr;
+    for (int t0 = wbeg + lane * 8; t0 - lane * 8 < wend && cnt != 0; t0 += 256) {
+      uint32_t ltm, eqm;
+      masks(t0, ltm, eqm);
+      if (__ballot_sync(kFull, (ltm | eqm) != 0) == 0) continue;
+      const unsigned packed = (unsigned)__popc(ltm) | ((unsigned)__popc(eqm) << 16);
+      unsigned incl = packed;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const unsigned o = __shfl_up_sync(kFull, incl, m);
+        if (lane >= m) incl += o;
+      }
+      const unsigned excl = incl - packed;
+      const unsigned step_tot = __shfl_sync(kFull, incl, 31);
+      if (ltm | eqm) {
+        const int lt_before = run_lt + (int)(excl & 0xffffu), eq_before = run_eq + (int)(excl >> 16);
+        int pos = lt_before + min(eq_before, eq_budget);
+        int eq_seen = eq_before;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          bool take = (ltm >> e) & 1u;
+          if ((eqm >> e) & 1u) take = eq_seen++ < eq_budget;
+          if (take) {
+            const int tok = (int)start + t0 + e;
+            if (pos < selcap) sel[g * selcap + pos] = tok;
+            if (idx_row) idx_row[pos] = tok;
+            ++pos;
+          }
+        }
+      }
+      run_lt += (int)(step_tot & 0xffffu);
+      run_eq += (int)(step_tot >> 16);
+    }
+    if (sub == 0 && lane == 0) nsel[g] = min(tot_lt + min(tot_eq, eq_budget), selcap);  // rows to attend
+    if (rank == 0 && p.idx && sub == 0) {  // estimator.cpp:80 caps the selection at S
+      int32_t* row = p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget;
+      for (int i = k_eff + lane; i < p.budget; i += 32) row[i] = -1;
+    }
   }
   __syncthreads();
+  ADAMAS_TRACE(8);
 
   // ---------------------------------------------------------------- attend
   {
     constexpr int WG = kFusedWarps / G;  // warps per q-head
     const int g = warp % G, sub = warp / G;
-    const int nsel = scal[48 + g];
+    const int ns = nsel[g];
     const int hq = hk * G + g;
     const T* qp = reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + hq) * kHeadDim;
     float qf[4];
@@ -327,12 +434,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     const T* Vh = reinterpret_cast<const T*>(p.seq[si].V) + (int64_t)hk * cap * kHeadDim + lane * 4;
     float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
     constexpr int B = 4;  // rows in flight per warp
-    for (int r0 = sub; r0 < nsel; r0 += WG * B) {
+    for (int r0 = sub; r0 < ns; r0 += WG * B) {
       typename Raw4<T>::V kr[B], vr[B];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const int r = r0 + b * WG;
-        if (r < nsel) {
+        if (r < ns) {
           const int64_t t = sel[g * selcap + r];
           kr[b] = Raw4<T>::load(Kh + t * kHeadDim);
           vr[b] = Raw4<T>::load(Vh + t * kHeadDim);
@@ -341,7 +448,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const int r = r0 + b * WG;
-        if (r < nsel) {
+        if (r < ns) {
           float kf[4], vf[4];
           Raw4<T>::to_float(kr[b], kf);
           Raw4<T>::to_float(vr[b], vf);
@@ -356,6 +463,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
         }
       }
     }
+    ADAMAS_TRACE(9);
     float* wp = wpart + warp * kPartStride;
     if (lane == 0) { wp[0] = m; wp[1] = l; }
 #pragma unroll
@@ -363,22 +471,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     __syncthreads();
     if (sub == 0) {  // combine this head's WG warp partials, push to the merging rank
       float M = -INFINITY;
-      for (int s2 = 0; s2 < WG; ++s2) M = fmaxf(M, wpart[(s2 * G + g) * kPartStride]);
+      for (int s2 = 0; s2 < WG; ++s2) {
+        const float* q2 = wpart + (s2 * G + g) * kPartStride;
+        if (q2[1] > 0.f) M = fmaxf(M, q2[0]);
+      }
       float Lsum = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
       for (int s2 = 0; s2 < WG; ++s2) {
         const float* q2 = wpart + (s2 * G + g) * kPartStride;
-        if (q2[1] == 0.f) continue;
+        if (!(q2[1] > 0.f)) continue;
         const float c = exp2f(q2[0] - M);
         Lsum += q2[1] * c;
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[j] += q2[4 + lane * 4 + j] * c;
       }
-      float* dst = cluster.map_shared_rank(inbox, g % C) + (rank * G + g) * kPartStride;
-      if (lane == 0) { dst[0] = M; dst[1] = Lsum; }
-      *reinterpret_cast<float4*>(dst + 4 + lane * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      // push (M, L, o[128]) into the merging rank's inbox[rank][g] (528 B)
+      const uint32_t local = smem_addr(inbox + (rank * G + g) * kPartStride);
+      const uint32_t dst = mapa_shared(local, (uint32_t)(g % C));
+      const uint32_t bar = mapa_shared(smem_addr(inbox_bar), (uint32_t)(g % C));
+      if (lane == 0) st_async_v4(dst, __float_as_uint(M), __float_as_uint(Lsum), 0u, 0u, bar);
+      st_async_v4(dst + 16 + lane * 16, __float_as_uint(acc[0]), __float_as_uint(acc[1]), __float_as_uint(acc[2]),
+                  __float_as_uint(acc[3]), bar);
     }
   }
-  cluster.sync();  // #2: partials delivered; no rank touches remote smem after this
+  ADAMAS_TRACE(10);
+  if (n_owned) mbar_wait(inbox_bar, 0);  // all C partials of the heads this rank merges
+  ADAMAS_TRACE(11);
 
   // ---------------------------------------------------------------- merge
   for (int g = warp; g < G; g += kFusedWarps) {
@@ -394,13 +511,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
       if (!(q2[1] > 0.f)) continue;
       const float c = exp2f(q2[0] - M);
       Lsum += q2[1] * c;
-      const float4 v = *reinterpret_cast<const float4*>(q2 + 4 + lane * 4);
-      acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
+      const float4 v4 = *reinterpret_cast<const float4*>(q2 + 4 + lane * 4);
+      acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
     }
     const float inv = 1.f / Lsum;
     float* op = p.out + ((int64_t)si * n_q + (int64_t)hk * G + g) * kHeadDim + lane * 4;
     *reinterpret_cast<float4*>(op) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
   }
+  ADAMAS_TRACE(12);
 }
 
 }  // namespace adamas_dev

@@ -14,8 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _lib():
-    from paper_2510_18413_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     from paper_2510_18413_b200._lib import load
     return load()
 

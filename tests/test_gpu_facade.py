@@ -10,8 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_facade_driver(gpu):
-    from paper_2510_18413_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     exe = os.path.join(ROOT, "tests", "cpp", "facade_tests")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout, r.stderr)

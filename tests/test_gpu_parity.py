@@ -27,6 +27,9 @@ def test_encode_append_codes_bit_exact(gpu, oracle, bf16):
     K, V, _ = make_inputs(S, n_kv, n_kv, bf16, 11)
     K[7] *= 1e-30  # tiny and huge scales
     K[8] *= 1e30 if not bf16 else 1e20
+    if bf16:
+        from oracle.bindings import bf16_round
+        K = bf16_round(K)
     cache = fill_cache(gpu, K, V, bf16)
     assert cache.seq_len == S
     words = cache.code_words().cpu().numpy().view(np.uint16)
@@ -199,3 +202,35 @@ def test_cuda_path_reproduces_reference_golden(gpu, golden, name):
     keep = min(budget, S)
     assert np.array_equal(idx.cpu().numpy()[:, :keep], golden[f"{name}/idx"])
     assert rel_err(out.cpu().numpy(), golden[f"{name}/out"]).max() <= TOL[bool(bf16)]
+
+
+def test_fused_decode_exact_encode_path(gpu, oracle, monkeypatch):
+    """The fused kernel's low-latency sigma (shuffle-tree sum with a near-tie
+    guard) and the sequential-sum path give identical codes and selections."""
+    monkeypatch.setenv("ADAMAS_EXACT_ENCODE", "1")
+    run_decode(gpu, oracle, 3000, 2, 4, 64, True, seed=31, steps=3)
+
+
+def test_fast_encode_near_ties_and_scales(gpu, oracle):
+    """Query vectors built to sit on the +/- kQ28 sigma thresholds after the
+    transform, plus extreme scales, through the fused decode step."""
+    from oracle.bindings import bf16_round
+    rng = np.random.default_rng(5)
+    S, budget = 600, 32
+    K, V, _ = make_inputs(S, 1, 1, False, 41)
+    cache = fill_cache(gpu, K[:-1], V[:-1], False, capacity=S + 64)
+    H = np.array([[1.0]])
+    for _ in range(7):
+        H = np.block([[H, H], [H, -H]])
+    H /= np.sqrt(128.0)
+    for trial in range(24):
+        y = rng.standard_normal(128)
+        sigma = np.sqrt(np.mean(y * y))
+        y[trial % 128] = 0.6744897501960817 * sigma * (1 if trial % 2 else -1)
+        q = (H @ y).astype(np.float32) * np.float32(10.0 ** ((trial % 9) - 4))
+        q = q.reshape(1, 128)
+        out, idx = cache.decode_step(to_dev(q, False), to_dev(K[-1], False), to_dev(V[-1], False), budget)
+        Kt = np.concatenate([K[:-1], K[-1:]])  # cache + appended token
+        _, _, eidx, eout = oracle_decode(oracle, Kt, np.concatenate([V[:-1], V[-1:]]), q, budget)
+        assert np.array_equal(idx.cpu().numpy(), eidx), trial
+        cache.truncate(S - 1)

@@ -1,0 +1,55 @@
+"""Per-phase timing of the fused decode kernel (globaltimer stamps per CTA).
+
+    python tools/phase_profile.py [--heads 32 --kv-heads 32 --seq 32768 --budget 128 --cluster 4]
+Prints mean / max over CTAs of each phase's duration (us) for one layer's launch.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--heads", type=int, default=32)
+ap.add_argument("--kv-heads", type=int, default=32)
+ap.add_argument("--seq", type=int, default=32768)
+ap.add_argument("--budget", type=int, default=128)
+ap.add_argument("--layers", type=int, default=8)
+ap.add_argument("--cluster", default="")
+args = ap.parse_args()
+if args.cluster:
+    os.environ["ADAMAS_CLUSTER"] = args.cluster
+import paper_2510_18413_b200 as ad  # noqa: E402
+from paper_2510_18413_b200._lib import load  # noqa: E402
+
+L = load()
+g = torch.Generator(device="cuda").manual_seed(0)
+caches = []
+for _ in range(args.layers):
+    c = ad.KvCache(args.kv_heads, args.seq + 1, torch.bfloat16)
+    for s0 in range(0, args.seq - 1, 4096):
+        n = min(4096, args.seq - 1 - s0)
+        c.update(torch.randn((n, args.kv_heads, 128), generator=g, device="cuda").bfloat16(),
+                 torch.randn((n, args.kv_heads, 128), generator=g, device="cuda").bfloat16())
+    caches.append(c)
+q = torch.randn((args.heads, 128), device="cuda").bfloat16()
+k = torch.randn((args.kv_heads, 128), device="cuda").bfloat16()
+trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+names = ["tma+zero", "encode", "scan", "cluster_sync1", "dsmem_hist", "thr_scan", "compact_p1", "compact_p2", "attend_gather", "attend_merge", "cluster_sync2", "merge"]
+for rep in range(3):
+    for c in caches:  # layers back to back, the last one is traced
+        L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if c is caches[-1] else None)
+        c.decode_step(q, k, k, args.budget)
+        c.truncate(args.seq - 1)
+    torch.cuda.synchronize()
+L.adamas_debug_trace(None)
+t = trace.view(-1, 16).cpu()
+n = int((t[:, 0] > 0).sum())
+t = t[:n].double()
+t0 = t[:, 0].min()
+print(f"CTAs {n}; launch span {(t[:, 12].max() - t0) / 1000:.2f} us; first start->last start {(t[:, 0].max() - t0) / 1000:.2f} us")
+for i, nm in enumerate(names):
+    d = (t[:, i + 1] - t[:, i]) / 1000
+    print(f"{nm:14s} mean {d.mean():7.2f} us  max {d.max():7.2f} us  min {d.min():7.2f}")
