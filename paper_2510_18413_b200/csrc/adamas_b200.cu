@@ -212,6 +212,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       prm.budget = (int)budget;
       prm.stages = stages;
       prm.exact_encode = env_int("ADAMAS_EXACT_ENCODE", 0);
+      prm.dbg = env_int("ADAMAS_DBG", 0);
       prm.q = q;
       prm.k_new = k_new;
       prm.v_new = v_new;

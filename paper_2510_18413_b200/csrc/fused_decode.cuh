@@ -52,6 +52,7 @@ struct FusedSeq {
 struct FusedParams {
   int n_seqs, n_kv, C, chunk, budget, stages;
   int exact_encode;  // 1: always the sequential fp64 sum (diagnostics / tests)
+  int dbg;           // diagnostics only: bit0 no L2 prefetch, bit1 no idx stores, bit2 skip pass 2
   const void* q;      // [n_seqs][n_q][128]
   const void* k_new;  // [n_seqs][n_kv][128]
   const void* v_new;
@@ -63,26 +64,36 @@ struct FusedParams {
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+  // SM cycle counter: exact within a CTA (phase durations), not across SMs
+  return (unsigned long long)clock64();
 }
-#define ADAMAS_TRACE(i) \
-  do { if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (i)] = global_ns(); } while (0)
+// BAR.SYNC on sm_100 blocks lazily (at the next access to barrier-protected
+// state), so a stamp taken right after __syncthreads() would record the
+// barrier's issue, not its release: the volatile shared load forces the wait.
+#define ADAMAS_TRACE(i)                                                              \
+  do {                                                                               \
+    if (p.trace != nullptr && threadIdx.x == 0) {                                    \
+      __shared__ volatile int trace_sink;                                            \
+      const int sink = trace_sink;                                                   \
+      p.trace[blockIdx.x * 16 + (i)] = global_ns() + (unsigned long long)(sink & 0); \
+    }                                                                                \
+  } while (0)
 
 // Dynamic shared-memory carve-up, identical on host and device.
 struct FusedSmem {
-  uint32_t stage, dist, hist, hist_all, sel, inbox, wpart, qcode, sq, bars, total;
+  uint32_t stage, dist, gmin, hist, hist_all, sel, inbox, wpart, qf, qcode, sq, bars, total;
   __host__ __device__ static uint32_t align(uint32_t x, uint32_t a) { return (x + a - 1u) & ~(a - 1u); }
   __host__ __device__ FusedSmem(int G, int C, int chunk, int selcap, int stages) {
     uint32_t o = 0;
     stage = o; o += (uint32_t)stages * kStageBytes;
     dist = o;  o = align(o + (uint32_t)G * chunk * 2, 16);
+    gmin = o;  o = align(o + (uint32_t)G * (chunk / 32) * 2, 16);  // min distance per 32-token group
     hist = o;  o += (uint32_t)G * kHistBins * 4;
     hist_all = o; o += (uint32_t)C * G * kHistBins * 2;  // u16 histograms received from every rank
     sel = o;   o = align(o + (uint32_t)G * selcap * 4, 16);
     inbox = o; o += (uint32_t)C * G * kPartStride * 4;
     wpart = o; o += kFusedWarps * kPartStride * 4;
+    qf = o;    o += (uint32_t)G * kHeadDim * 4;  // the G query heads as fp32
     o = align(o, 32);
     qcode = o; o += (uint32_t)(G + 1) * 32;
     sq = o;    o += (uint32_t)(G + 1) * kHeadDim * 8;
@@ -131,7 +142,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int scan_scratch[2 * kMaxG * kFusedWarps];
   __shared__ int sc[kMaxG][4];  // per q-head: T, below, pre_lt, pre_eq
-  __shared__ int warp_cnt[kFusedWarps][2];
   __shared__ int nsel[kMaxG];
   const int C = p.C;
   const int rank = (int)cluster_rank();
@@ -154,11 +164,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
   const FusedSmem L(G, C, p.chunk, selcap, ring);
   uint4* stage = reinterpret_cast<uint4*>(smem + L.stage);
   uint16_t* dist = reinterpret_cast<uint16_t*>(smem + L.dist);
+  uint16_t* gmin = reinterpret_cast<uint16_t*>(smem + L.gmin);
+  const int ngroups_cap = p.chunk / 32;
   int* hist = reinterpret_cast<int*>(smem + L.hist);
   uint16_t* hist_all = reinterpret_cast<uint16_t*>(smem + L.hist_all);
   int* sel = reinterpret_cast<int*>(smem + L.sel);
   float* inbox = reinterpret_cast<float*>(smem + L.inbox);
   float* wpart = reinterpret_cast<float*>(smem + L.wpart);
+  float* qfs = reinterpret_cast<float*>(smem + L.qf);
   Code* qcode = reinterpret_cast<Code*>(smem + L.qcode);
   double* sqs = reinterpret_cast<double*>(smem + L.sq);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -196,12 +209,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     if (n_owned) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
   }
   for (int i = tid; i < G * kHistBins; i += kFusedThreads) hist[i] = 0;
+  for (int i = tid; i < G * ngroups_cap; i += kFusedThreads) gmin[i] = 0xffff;
   ADAMAS_TRACE(1);
 
   if (warp < G) {  // encode query head hk * G + warp (sweep.cpp:92-94)
     const T* qp = reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + (int64_t)hk * G + warp) * kHeadDim;
     float f[4];
     Raw4<T>::to_float(Raw4<T>::load(qp + lane * 4), f);
+    *reinterpret_cast<float4*>(qfs + warp * kHeadDim + lane * 4) = make_float4(f[0], f[1], f[2], f[3]);
     Code c;
     if (!encode128_warp(f, sqs + warp * kHeadDim, c, !p.exact_encode) && lane == 0)
       atomicOr(p.status, kStatusDegenerate);
@@ -250,14 +265,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int j = tid + u * kFusedThreads;
-      if (j < ntok) {
-        const uint32_t lo[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, hi[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+      const bool valid = j < ntok;
+      const uint32_t lo[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, hi[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const uint32_t d = l1_distance(qc[g], lo, hi);
+      for (int g = 0; g < G; ++g) {
+        const uint32_t d = valid ? l1_distance(qc[g], lo, hi) : 0xffffu;
+        if (valid) {
           dist[g * p.chunk + base + j] = (uint16_t)d;
           atomicAdd(&hist[g * kHistBins + d], 1);
         }
+        // per 32-token group minimum: lets the compaction skip groups above T
+        const uint32_t m = __reduce_min_sync(kFull, d);
+        if (lane == 0 && (base + j) < p.chunk) gmin[g * ngroups_cap + ((base + j) >> 5)] = (uint16_t)m;
       }
     }
     __syncthreads();
@@ -266,8 +285,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
   if (has_new && tid < G) {  // the appended token is a candidate
     const Code nc = qcode[G];
     const uint32_t d = l1_distance(make_qcode(qcode[tid]), nc.lo, nc.hi);
-    dist[tid * p.chunk + (int)(s_old - start)] = (uint16_t)d;
+    const int lt = (int)(s_old - start);
+    dist[tid * p.chunk + lt] = (uint16_t)d;
     atomicAdd(&hist[tid * kHistBins + d], 1);
+    uint16_t& gm = gmin[tid * ngroups_cap + (lt >> 5)];
+    gm = (uint16_t)min((uint32_t)gm, d);
   }
   ADAMAS_TRACE(3);
   __syncthreads();  // local histogram final
@@ -288,32 +310,49 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
   ADAMAS_TRACE(4);
 
   // ---------------------------------------------------------------- threshold
-  // thread t owns distance bin t of every q-head
+  // Warp g (g < G) finds head g's threshold T = smallest distance whose
+  // cumulative count over all ranks reaches k: lane l owns bins 16l..16l+15,
+  // a warp scan orders the lanes, the owning lane walks its 16 bins.
   const int k_eff = (int)min((int64_t)p.budget, S);
-  {
-    int tot[G], pre[G];
+  if (warp < G) {
+    const int g = warp;
+    int tot[16], pre[16];
 #pragma unroll
-    for (int g = 0; g < G; ++g) { tot[g] = 0; pre[g] = 0; }
+    for (int i = 0; i < 16; ++i) { tot[i] = 0; pre[i] = 0; }
     for (int r = 0; r < C; ++r) {
+      const uint4* h = reinterpret_cast<const uint4*>(hist_all + ((size_t)r * G + g) * kHistBins + lane * 16);
+      const uint4 a = h[0], b = h[1];
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int h = hist_all[((size_t)r * G + g) * kHistBins + tid];
-        tot[g] += h;
-        pre[g] += r < rank ? h : 0;
+      for (int i = 0; i < 16; ++i) {
+        const int v = (int)((w[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+        tot[i] += v;
+        pre[i] += r < rank ? v : 0;
       }
     }
-    ADAMAS_TRACE(5);
-    int v[2 * G], ex[2 * G], sum[2 * G];
+    int lt = 0, lp = 0;
 #pragma unroll
-    for (int g = 0; g < G; ++g) { v[g] = tot[g]; v[G + g] = pre[g]; }
-    block_scan<2 * G>(v, ex, sum, scan_scratch);
+    for (int i = 0; i < 16; ++i) { lt += tot[i]; lp += pre[i]; }
+    int it = lt, ip = lp;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (ex[g] < k_eff && ex[g] + tot[g] >= k_eff) {  // this bin holds the k-th smallest
-        sc[g][0] = tid;        // T
-        sc[g][1] = ex[g];      // count of distances < T over the whole head
-        sc[g][2] = ex[G + g];  // count of distances < T in ranks before this one
-        sc[g][3] = pre[g];     // count of distances == T in ranks before this one
+    for (int m = 1; m < 32; m <<= 1) {
+      const int a2 = __shfl_up_sync(kFull, it, m), b2 = __shfl_up_sync(kFull, ip, m);
+      if (lane >= m) { it += a2; ip += b2; }
+    }
+    int c = it - lt, cp = ip - lp;  // exclusive: counts in lower bins
+    if (c < k_eff && c + lt >= k_eff) {
+      bool done = false;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (!done && c + tot[i] >= k_eff) {
+          sc[g][0] = lane * 16 + i;  // T
+          sc[g][1] = c;              // count of distances < T over the whole head
+          sc[g][2] = cp;             // count of distances < T in ranks before this one
+          sc[g][3] = pre[i];         // count of distances == T in ranks before this one
+          done = true;
+        }
+        c += tot[i];
+        cp += pre[i];
       }
     }
   }
@@ -321,98 +360,105 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
   ADAMAS_TRACE(6);
 
   // ---------------------------------------------------------------- compaction
-  // Warp w serves q-head g = w % G over sub-range w / G of this rank's tokens;
-  // lane l reads 8 consecutive distances per 256-token step, so the
-  // (sub-range, step, lane) order is index order. Pass 1 counts (< T, == T)
-  // per warp; pass 2 re-walks with a packed warp scan and emits in order.
+  // Thread t of head g (TG = 512 / G threads per head) owns a contiguous run
+  // of 32-token groups; a group whose minimum distance exceeds T holds no
+  // selected token and costs one shared load. Candidate groups are evaluated
+  // with SWAR on u16 pairs: (K - x) & 0x80008000 has a guard bit set exactly
+  // where x <= thr (K = thr in both halves | 0x80008000; distances < 2^15).
+  // Count -> one CTA scan in index order -> emit.
   {
-    constexpr int WG = kFusedWarps / G;
-    const int g = warp % G, sub = warp / G;
-    const int per_warp = ((len + WG - 1) / WG + 255) / 256 * 256;
-    const int wbeg = sub * per_warp, wend = min(len, wbeg + per_warp);
+    constexpr int TG = kFusedThreads / G;
+    const int g = tid / TG, t_in = tid % TG;
+    const int ngroups = (len + 31) >> 5;
+    const int gpt = (ngroups + TG - 1) / TG;
+    const int grp0 = min(ngroups, t_in * gpt), grp1 = min(ngroups, grp0 + gpt);
     const int thr = sc[g][0], below = sc[g][1], pre_lt = sc[g][2], pre_eq = sc[g][3];
     const int need = k_eff - below;               // ties at T the whole head takes
     const int eq_budget = max(0, need - pre_eq);  // ... of which this rank may take
     const int out_off = pre_lt + min(pre_eq, need);
     const uint16_t* dg = dist + g * p.chunk;
-    auto masks = [&](int t0, uint32_t& ltm, uint32_t& eqm) {
-      ltm = 0;
-      eqm = 0;
-      if (t0 < wend) {
-        const uint4 vv = *reinterpret_cast<const uint4*>(dg + t0);
-        const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+    const uint16_t* gm = gmin + g * ngroups_cap;
+    const uint32_t kle = ((uint32_t)thr * 0x00010001u) | 0x80008000u;  // x <= thr
+    const uint32_t klt = thr > 0 ? (((uint32_t)(thr - 1) * 0x00010001u) | 0x80008000u) : 0u;  // x < thr
+    // 32-bit masks (bit i = token i of the group) of x < thr and x == thr
+    auto group_masks = [&](int grp, uint32_t& ltm, uint32_t& eqm) {
+      const uint4* src = reinterpret_cast<const uint4*>(dg + grp * 32);
+      uint32_t le = 0, lt = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int d = (int)((w[e >> 1] >> (16 * (e & 1))) & 0xffffu);
-          const bool valid = t0 + e < wend;
-          ltm |= (uint32_t)(valid && d < thr) << e;
-          eqm |= (uint32_t)(valid && d == thr) << e;
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint4 v4 = src[q4];
+        const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = (q4 * 4 + e) * 2;
+          const uint32_t a = (kle - w[e]) & 0x80008000u, b = thr > 0 ? ((klt - w[e]) & 0x80008000u) : 0u;
+          le |= ((a >> 15) & 1u) << i | (a >> 31) << (i + 1);
+          lt |= ((b >> 15) & 1u) << i | (b >> 31) << (i + 1);
         }
       }
+      const int valid = len - grp * 32;  // tokens of this group inside the rank's range
+      const uint32_t vm = valid >= 32 ? 0xffffffffu : ((1u << valid) - 1u);
+      ltm = lt & vm;
+      eqm = (le & ~lt) & vm;
     };
     const T* Kg = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
     const T* Vg = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
-    unsigned cnt = 0;  // packed: lt in bits 0..15, eq in bits 16..31
-    for (int t0 = wbeg + lane * 8; t0 - lane * 8 < wend; t0 += 256) {
+    int my_lt = 0, my_eq = 0;
+    for (int grp = grp0; grp < grp1; ++grp) {
+      if (gm[grp] > thr) continue;
       uint32_t ltm, eqm;
-      masks(t0, ltm, eqm);
-      cnt += (unsigned)__popc(ltm) | ((unsigned)__popc(eqm) << 16);
-      // candidates (d <= T): start pulling their K and V rows into L2 now, so
-      // the gather after the compaction hits L2 instead of HBM
-      for (uint32_t m = ltm | eqm; m; m &= m - 1) {
-        const int t = t0 + __ffs(m) - 1;
-        prefetch_l2_bulk(Kg + (int64_t)t * kHeadDim, kHeadDim * sizeof(T));
-        prefetch_l2_bulk(Vg + (int64_t)t * kHeadDim, kHeadDim * sizeof(T));
-      }
-    }
-    cnt = __reduce_add_sync(kFull, cnt);
-    if (lane == 0) { warp_cnt[warp][0] = (int)(cnt & 0xffffu); warp_cnt[warp][1] = (int)(cnt >> 16); }
-    __syncthreads();
-    ADAMAS_TRACE(7);
-    int run_lt = 0, run_eq = 0, tot_lt = 0, tot_eq = 0;
-    for (int s2 = 0; s2 < WG; ++s2) {
-      const int w2 = s2 * G + g;
-      if (s2 < sub) { run_lt += warp_cnt[w2][0]; run_eq += warp_cnt[w2][1]; }
-      tot_lt += warp_cnt[w2][0];
-      tot_eq += warp_cnt[w2][1];
-    }
-    int32_t* idx_row = p.idx ? p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off : nullptr;
-    for (int t0 = wbeg + lane * 8; t0 - lane * 8 < wend && cnt != 0; t0 += 256) {
-      uint32_t ltm, eqm;
-      masks(t0, ltm, eqm);
-      if (__ballot_sync(kFull, (ltm | eqm) != 0) == 0) continue;
-      const unsigned packed = (unsigned)__popc(ltm) | ((unsigned)__popc(eqm) << 16);
-      unsigned incl = packed;
+      group_masks(grp, ltm, eqm);
+      my_lt += __popc(ltm);
+      my_eq += __popc(eqm);
+      for (uint32_t m = (p.dbg & 1) ? 0u : (ltm | eqm); m; m &= m - 1) {  // warm L2 for the gather
+        const int t = grp * 32 + __ffs(m) - 1;
+        const char* kp = reinterpret_cast<const char*>(Kg + (int64_t)t * kHeadDim);
+        const char* vp = reinterpret_cast<const char*>(Vg + (int64_t)t * kHeadDim);
 #pragma unroll
-      for (int m = 1; m < 32; m <<= 1) {
-        const unsigned o = __shfl_up_sync(kFull, incl, m);
-        if (lane >= m) incl += o;
-      }
-      const unsigned excl = incl - packed;
-      const unsigned step_tot = __shfl_sync(kFull, incl, 31);
-      if (ltm | eqm) {
-        const int lt_before = run_lt + (int)(excl & 0xffffu), eq_before = run_eq + (int)(excl >> 16);
-        int pos = lt_before + min(eq_before, eq_budget);
-        int eq_seen = eq_before;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          bool take = (ltm >> e) & 1u;
-          if ((eqm >> e) & 1u) take = eq_seen++ < eq_budget;
-          if (take) {
-            const int tok = (int)start + t0 + e;
-            if (pos < selcap) sel[g * selcap + pos] = tok;
-            if (idx_row) idx_row[pos] = tok;
-            ++pos;
-          }
+        for (int c = 0; c < (int)(kHeadDim * sizeof(T)); c += 128) {
+          prefetch_l2(kp + c);
+          prefetch_l2(vp + c);
         }
       }
-      run_lt += (int)(step_tot & 0xffffu);
-      run_eq += (int)(step_tot >> 16);
     }
-    if (sub == 0 && lane == 0) nsel[g] = min(tot_lt + min(tot_eq, eq_budget), selcap);  // rows to attend
-    if (rank == 0 && p.idx && sub == 0) {  // estimator.cpp:80 caps the selection at S
+    int lt_before = 0, eq_before = 0;
+    {
+      int v[2 * G], ex[2 * G], sum[2 * G];
+#pragma unroll
+      for (int g2 = 0; g2 < G; ++g2) { v[2 * g2] = g2 == g ? my_lt : 0; v[2 * g2 + 1] = g2 == g ? my_eq : 0; }
+      block_scan<2 * G>(v, ex, sum, scan_scratch);
+#pragma unroll
+      for (int g2 = 0; g2 < G; ++g2) {
+        if (g2 == g) { lt_before = ex[2 * g2]; eq_before = ex[2 * g2 + 1]; }
+        if (tid == 0) nsel[g2] = min(sum[2 * g2] + min(sum[2 * g2 + 1], max(0, k_eff - sc[g2][1] - sc[g2][3])), selcap);
+      }
+    }
+    ADAMAS_TRACE(7);
+    if (my_lt | my_eq) {
+      int32_t* idx_row = (p.idx && !(p.dbg & 2))
+                             ? p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off
+                             : nullptr;
+      int pos = lt_before + min(eq_before, eq_budget);
+      int eq_seen = eq_before;
+      for (int grp = grp0; grp < grp1; ++grp) {
+        if (gm[grp] > thr) continue;
+        uint32_t ltm, eqm;
+        group_masks(grp, ltm, eqm);
+        for (uint32_t m = ltm | eqm; m; m &= m - 1) {
+          const int i = __ffs(m) - 1;
+          if ((eqm >> i) & 1u) {
+            if (eq_seen++ >= eq_budget) continue;  // ties beyond the budget are not taken
+          }
+          const int tok = (int)start + grp * 32 + i;
+          if (pos < selcap) sel[g * selcap + pos] = tok;
+          if (idx_row) idx_row[pos] = tok;
+          ++pos;
+        }
+      }
+    }
+    if (rank == 0 && p.idx && t_in == 0) {  // estimator.cpp:80 caps the selection at S
       int32_t* row = p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget;
-      for (int i = k_eff + lane; i < p.budget; i += 32) row[i] = -1;
+      for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
     }
   }
   __syncthreads();
@@ -424,9 +470,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     const int g = warp % G, sub = warp / G;
     const int ns = nsel[g];
     const int hq = hk * G + g;
-    const T* qp = reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + hq) * kHeadDim;
-    float qf[4];
-    Raw4<T>::to_float(Raw4<T>::load(qp + lane * 4), qf);
+    const float4 q4 = *reinterpret_cast<const float4*>(qfs + g * kHeadDim + lane * 4);
+    float qf[4] = {q4.x, q4.y, q4.z, q4.w};
     const float scale = 0.088388347648318440f * kLog2e;  // 1/sqrt(128), log2 units
 #pragma unroll
     for (int j = 0; j < 4; ++j) qf[j] *= scale;
@@ -470,19 +515,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     for (int j = 0; j < 4; ++j) wp[4 + lane * 4 + j] = o[j];
     __syncthreads();
     if (sub == 0) {  // combine this head's WG warp partials, push to the merging rank
-      float M = -INFINITY;
-      for (int s2 = 0; s2 < WG; ++s2) {
-        const float* q2 = wpart + (s2 * G + g) * kPartStride;
-        if (q2[1] > 0.f) M = fmaxf(M, q2[0]);
-      }
-      float Lsum = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int s2 = 0; s2 < WG; ++s2) {
-        const float* q2 = wpart + (s2 * G + g) * kPartStride;
-        if (!(q2[1] > 0.f)) continue;
-        const float c = exp2f(q2[0] - M);
-        Lsum += q2[1] * c;
+      const float* mine = wpart + (lane * G + g) * kPartStride;
+      const float ml = lane < WG ? mine[0] : -INFINITY, ll = lane < WG ? mine[1] : 0.f;
+      float M = ll > 0.f ? ml : -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] += q2[4 + lane * 4 + j] * c;
+      for (int m2 = 16; m2 > 0; m2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, m2));
+      const float cl = ll > 0.f ? exp2f(ml - M) : 0.f;
+      const float Lsum = warp_sum(ll * cl);
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s2 = 0; s2 < WG; ++s2) {
+        const float c = __shfl_sync(kFull, cl, s2);
+        const float4 v4 = *reinterpret_cast<const float4*>(wpart + (s2 * G + g) * kPartStride + 4 + lane * 4);
+        acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
       }
       // push (M, L, o[128]) into the merging rank's inbox[rank][g] (528 B)
       const uint32_t local = smem_addr(inbox + (rank * G + g) * kPartStride);

@@ -36,7 +36,7 @@ for _ in range(args.layers):
     caches.append(c)
 q = torch.randn((args.heads, 128), device="cuda").bfloat16()
 k = torch.randn((args.kv_heads, 128), device="cuda").bfloat16()
-trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+trace = torch.zeros(4096 * 16 + 4096 * 16 * 4, dtype=torch.int64, device="cuda")
 names = ["tma+zero", "encode", "scan", "cluster_sync1", "dsmem_hist", "thr_scan", "compact_p1", "compact_p2", "attend_gather", "attend_merge", "cluster_sync2", "merge"]
 for rep in range(3):
     for c in caches:  # layers back to back, the last one is traced
@@ -45,11 +45,23 @@ for rep in range(3):
         c.truncate(args.seq - 1)
     torch.cuda.synchronize()
 L.adamas_debug_trace(None)
-t = trace.view(-1, 16).cpu()
+wt = trace[4096 * 16:].view(4096, 16, 4).cpu().double()
+t = trace[:4096 * 16].view(-1, 16).cpu()
 n = int((t[:, 0] > 0).sum())
 t = t[:n].double()
-t0 = t[:, 0].min()
-print(f"CTAs {n}; launch span {(t[:, 12].max() - t0) / 1000:.2f} us; first start->last start {(t[:, 0].max() - t0) / 1000:.2f} us")
+GHZ = float(os.environ.get("SM_GHZ", "1.965"))  # clock64 stamps -> us
+t = t / (GHZ * 1000.0)
+print(f"CTAs {n}; per-CTA span mean {(t[:, 12] - t[:, 0]).mean():.2f} us max {(t[:, 12] - t[:, 0]).max():.2f} us")
+if os.environ.get("ADAMAS_DBG", "0") == "8":
+    d = t[:, 5] - t[:, 7]
+    print(f"  [bare barrier after p1: mean {d.mean():.2f} max {d.max():.2f}]")
+if int(os.environ.get("ADAMAS_DBG", "0")) & 16:
+    w = wt[:n] / (GHZ * 1000.0)
+    a = (w[:, :, 1] - w[:, :, 0])
+    b = (w[:, :, 2] - w[:, :, 1])
+    print(f"  [p2 per-warp: cnt-loop mean {a.mean():.3f} max {a.max():.3f}; emit mean {b.mean():.3f} max {b.max():.3f}]")
+    endw = w[:, :, 2]
+    print(f"  [p2 end spread within CTA: mean {(endw.max(1).values - endw.min(1).values).mean():.3f}]")
 for i, nm in enumerate(names):
-    d = (t[:, i + 1] - t[:, i]) / 1000
+    d = (t[:, i + 1] - t[:, i])
     print(f"{nm:14s} mean {d.mean():7.2f} us  max {d.max():7.2f} us  min {d.min():7.2f}")
