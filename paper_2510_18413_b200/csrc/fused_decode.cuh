@@ -63,6 +63,11 @@ struct FusedParams {
   FusedSeq seq[kMaxSeqs];
 };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned long long global_ns() {
   // SM cycle counter: exact within a CTA (phase durations), not across SMs
   return (unsigned long long)clock64();
@@ -186,6 +191,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
 
   // ---------------------------------------------------------------- prologue
   ADAMAS_TRACE(0);
+  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 16 + 14] = globaltimer_ns();
   const int n_stages = (mem_len + kStageTok - 1) / kStageTok;
   constexpr int kIssueWarp = kFusedWarps - 1;
   auto issue = [&](int st) {
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     }
   }
   __syncthreads();
-  ADAMAS_TRACE(6);
+  ADAMAS_TRACE(5);
 
   // ---------------------------------------------------------------- compaction
   // Thread t of head g (TG = 512 / G threads per head) owns a contiguous run
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
         if (tid == 0) nsel[g2] = min(sum[2 * g2] + min(sum[2 * g2 + 1], max(0, k_eff - sc[g2][1] - sc[g2][3])), selcap);
       }
     }
-    ADAMAS_TRACE(7);
+    ADAMAS_TRACE(6);
     if (my_lt | my_eq) {
       int32_t* idx_row = (p.idx && !(p.dbg & 2))
                              ? p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     }
   }
   __syncthreads();
-  ADAMAS_TRACE(8);
+  ADAMAS_TRACE(7);
 
   // ---------------------------------------------------------------- attend
   {
@@ -508,7 +514,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
         }
       }
     }
-    ADAMAS_TRACE(9);
+    ADAMAS_TRACE(8);
     float* wp = wpart + warp * kPartStride;
     if (lane == 0) { wp[0] = m; wp[1] = l; }
 #pragma unroll
@@ -538,9 +544,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
                   __float_as_uint(acc[3]), bar);
     }
   }
-  ADAMAS_TRACE(10);
+  ADAMAS_TRACE(9);
   if (n_owned) mbar_wait(inbox_bar, 0);  // all C partials of the heads this rank merges
-  ADAMAS_TRACE(11);
+  ADAMAS_TRACE(10);
 
   // ---------------------------------------------------------------- merge
   for (int g = warp; g < G; g += kFusedWarps) {
@@ -563,7 +569,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     float* op = p.out + ((int64_t)si * n_q + (int64_t)hk * G + g) * kHeadDim + lane * 4;
     *reinterpret_cast<float4*>(op) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
   }
-  ADAMAS_TRACE(12);
+  ADAMAS_TRACE(11);
+  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 16 + 15] = globaltimer_ns();
 }
 
 }  // namespace adamas_dev

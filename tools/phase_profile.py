@@ -37,7 +37,8 @@ for _ in range(args.layers):
 q = torch.randn((args.heads, 128), device="cuda").bfloat16()
 k = torch.randn((args.kv_heads, 128), device="cuda").bfloat16()
 trace = torch.zeros(4096 * 16 + 4096 * 16 * 4, dtype=torch.int64, device="cuda")
-names = ["tma+zero", "encode", "scan", "cluster_sync1", "dsmem_hist", "thr_scan", "compact_p1", "compact_p2", "attend_gather", "attend_merge", "cluster_sync2", "merge"]
+names = ["tma+zero", "encode+append", "scan", "hist_exchange", "threshold", "compact_count", "compact_emit",
+         "attend_gather", "attend_combine", "inbox_wait", "merge"]
 for rep in range(3):
     for c in caches:  # layers back to back, the last one is traced
         L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if c is caches[-1] else None)
@@ -48,10 +49,13 @@ L.adamas_debug_trace(None)
 wt = trace[4096 * 16:].view(4096, 16, 4).cpu().double()
 t = trace[:4096 * 16].view(-1, 16).cpu()
 n = int((t[:, 0] > 0).sum())
-t = t[:n].double()
+gt = t[:n, 14:16].double() / 1000.0  # globaltimer ns -> us
+print(f"globaltimer: CTA start spread {(gt[:, 0].max() - gt[:, 0].min()):.2f} us, first start -> last end "
+      f"{(gt[:, 1].max() - gt[:, 0].min()):.2f} us, end spread {(gt[:, 1].max() - gt[:, 1].min()):.2f} us")
+t = t[:n, :14].double()
 GHZ = float(os.environ.get("SM_GHZ", "1.965"))  # clock64 stamps -> us
 t = t / (GHZ * 1000.0)
-print(f"CTAs {n}; per-CTA span mean {(t[:, 12] - t[:, 0]).mean():.2f} us max {(t[:, 12] - t[:, 0]).max():.2f} us")
+print(f"CTAs {n}; per-CTA span mean {(t[:, 11] - t[:, 0]).mean():.2f} us max {(t[:, 11] - t[:, 0]).max():.2f} us")
 if os.environ.get("ADAMAS_DBG", "0") == "8":
     d = t[:, 5] - t[:, 7]
     print(f"  [bare barrier after p1: mean {d.mean():.2f} max {d.max():.2f}]")
