@@ -146,7 +146,9 @@ void adamas_debug_trace(unsigned long long* device_buffer);
 /* ---------------------------------------------------------------- host converters */
 
 /* Reference PackedCodes words <-> device bit-plane record (32 B), host memory,
- * n vectors of 128 codes. Lossless both ways. */
+ * n vectors of 128 codes: uint32 planes[8] per vector, words 0..3 the low code
+ * bits (element e at bit e/4 of word e%4), words 4..7 low XOR high bit.
+ * Lossless both ways. */
 void adamas_codes_ref_to_planes(const uint16_t* ref, int64_t n, uint32_t* planes);
 void adamas_codes_planes_to_ref(const uint32_t* planes, int64_t n, uint16_t* ref);
 

@@ -19,6 +19,10 @@ using namespace adamas_dev;
 struct adamas_cache {
   int n_kv = 0, head_dim = 0, bits = 0, dtype = 0, device = 0;
   int64_t capacity = 0, seq_len = 0;
+  // Tokens >= dirty_from were written by the most recent kernel that wrote
+  // this cache; a PDL-launched decode step streams only tokens below it before
+  // its grid-dependency wait.
+  int64_t dirty_from = 0;
   void* K = nullptr;
   void* V = nullptr;
   uint4* codes = nullptr;  // [n_kv][2 planes][capacity] x 16 B
@@ -112,7 +116,10 @@ int do_append(adamas_cache* c, const void* keys, const void* values, const uint1
   const int rc = c->dtype == ADAMAS_BF16
                      ? launch_append<__nv_bfloat16>(c, keys, values, codes_ref, n_tokens, as_stream(stream))
                      : launch_append<float>(c, keys, values, codes_ref, n_tokens, as_stream(stream));
-  if (rc == ADAMAS_OK) c->seq_len += n_tokens;
+  if (rc == ADAMAS_OK) {
+    c->dirty_from = c->seq_len;
+    c->seq_len += n_tokens;
+  }
   return rc;
 }
 
@@ -125,7 +132,7 @@ int check_heads(const adamas_cache* c, int n_q) {
 
 // ----------------------------------------------------------------- fused launcher
 template <typename T, int G>
-int launch_fused_t(const FusedParams& prm, int C, size_t smem, cudaStream_t s) {
+int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
   auto kern = fused_decode_kernel<T, G>;
   static bool configured = false;
   static size_t configured_smem = 0;
@@ -140,13 +147,29 @@ int launch_fused_t(const FusedParams& prm, int C, size_t smem, cudaStream_t s) {
   cfg.blockDim = dim3(kFusedThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // PDL only when every cluster is co-resident (one wave): dependents then
+  // occupy only SMs this grid does not need.
+  static int max_clusters[17] = {0};
+  if (prm.pdl) {
+    if (max_clusters[C] == 0) {
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = -1;
+      max_clusters[C] = n;
+    }
+    if ((int64_t)prm.n_seqs * prm.n_kv > max_clusters[C]) prm.pdl = 0;
+  }
+  if (prm.pdl) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   ADAMAS_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   return ADAMAS_OK;
 }
@@ -189,7 +212,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
     chunk = (chunk + 255) / 256 * 256;
     const int selcap = (int)std::min<int64_t>(budget, chunk);
     // one CTA per SM when the grid fits the machine, else two
-    const size_t smem_cap = (size_t)units * C <= (size_t)sm_count() ? 215 * 1024 : 108 * 1024;
+    const size_t smem_cap = (size_t)units * C <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
     const FusedSmem base(G, C, (int)chunk, selcap, 0);
     const int want = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (chunk + kStageTok - 1) / kStageTok));
     int stages = env_int("ADAMAS_STAGES", 0);
@@ -203,7 +226,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       C *= 2;
       continue;
     }
-    if (L.total <= smem_cap || (stages == 2 && L.total <= 215 * 1024)) {
+    if (L.total <= smem_cap || (stages == 2 && L.total <= 220 * 1024)) {
       FusedParams prm{};
       prm.n_seqs = n_seqs;
       prm.n_kv = n_kv;
@@ -213,6 +236,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       prm.stages = stages;
       prm.exact_encode = env_int("ADAMAS_EXACT_ENCODE", 0);
       prm.dbg = env_int("ADAMAS_DBG", 0);
+      prm.pdl = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
       prm.q = q;
       prm.k_new = k_new;
       prm.v_new = v_new;
@@ -226,6 +250,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
         prm.seq[i].V = caches[i]->V;
         prm.seq[i].cap = caches[i]->capacity;
         prm.seq[i].s_old = caches[i]->seq_len;
+        prm.seq[i].clean = std::min(caches[i]->dirty_from, caches[i]->seq_len);
       }
       return dtype == ADAMAS_BF16 ? launch_fused_dtype<__nv_bfloat16>(prm, G, C, L.total, s)
                                   : launch_fused_dtype<float>(prm, G, C, L.total, s);
@@ -447,7 +472,10 @@ int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const vo
     return ADAMAS_OK;
   }
   if (rc != ADAMAS_OK) return rc;
-  for (int i = 0; i < n_seqs; ++i) caches[i]->seq_len += 1;
+  for (int i = 0; i < n_seqs; ++i) {
+    caches[i]->dirty_from = caches[i]->seq_len;
+    caches[i]->seq_len += 1;
+  }
   return ADAMAS_OK;
 }
 
@@ -465,7 +493,7 @@ void adamas_codes_ref_to_planes(const uint16_t* ref, int64_t n, uint32_t* planes
     for (int e = 0; e < kHeadDim; ++e) {
       const uint32_t code = (b[e / 4] >> (2 * (e % 4))) & 3u;
       p[e % 4] |= (code & 1u) << (e / 4);
-      p[4 + e % 4] |= (code >> 1) << (e / 4);
+      p[4 + e % 4] |= ((code ^ (code >> 1)) & 1u) << (e / 4);  // x plane: lo ^ hi
     }
   }
 }
@@ -476,7 +504,8 @@ void adamas_codes_planes_to_ref(const uint32_t* planes, int64_t n, uint16_t* ref
     uint8_t* b = reinterpret_cast<uint8_t*>(ref + v * 16);
     for (int i = 0; i < 32; ++i) b[i] = 0;
     for (int e = 0; e < kHeadDim; ++e) {
-      const uint32_t code = ((p[e % 4] >> (e / 4)) & 1u) | (((p[4 + e % 4] >> (e / 4)) & 1u) << 1);
+      const uint32_t lo = (p[e % 4] >> (e / 4)) & 1u, x = (p[4 + e % 4] >> (e / 4)) & 1u;
+      const uint32_t code = lo | ((lo ^ x) << 1);
       b[e / 4] |= (uint8_t)(code << (2 * (e % 4)));
     }
   }

@@ -3,15 +3,15 @@
 // Code layout in HBM ("bit-plane", 32 B per token per kv-head at d = 128):
 //   two plane arrays per kv-head, each [capacity] x 16 B:
 //     lo plane of token t of kv-head h at planes[(2h + 0) * capacity + t]
-//     hi plane                         at planes[(2h + 1) * capacity + t]
+//     x  plane                         at planes[(2h + 1) * capacity + t]
 //   Element e (0..127) of the transformed key sits at bit (e / 4) of word
-//   e % 4 of the lo plane (low code bit) and of the hi plane (high bit).
-//   Separate planes make every per-lane 16-byte access (global or the
-//   bulk-copied shared-memory stage) contiguous across a warp.
+//   e % 4: the lo plane holds the code's low bit, the x plane holds
+//   low XOR high bit. Separate planes make every per-lane 16-byte access
+//   (global or the bulk-copied shared-memory stage) contiguous across a warp.
 // This is the reference PackedCodes (quantizer.hpp:44-50: element i at bits
 // [2(i%8), 2(i%8)+2) of u16 word i/8) with the bits transposed into planes, so
-// the Manhattan distance becomes ~3 LOP3 + 2 POPC per 32 elements instead of
-// the reference's nibble SWAR (kernels_scalar.cpp:41-70). Layout is an
+// the Manhattan distance becomes 2 LOP3 + ~1.25 POPC per 32 elements instead
+// of the reference's nibble SWAR (kernels_scalar.cpp:41-70). Layout is an
 // implementation freedom; the integer results are identical.
 #pragma once
 #include <cuda_bf16.h>
@@ -36,7 +36,7 @@ struct __align__(32) Code {
 
 // Query-side precomputation for the distance: X = lo ^ hi.
 struct QCode {
-  uint32_t lo[4], hi[4], x[4];
+  uint32_t lo[4], x[4];
 };
 
 __device__ __forceinline__ QCode make_qcode(const Code& c) {
@@ -44,26 +44,38 @@ __device__ __forceinline__ QCode make_qcode(const Code& c) {
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     q.lo[w] = c.lo[w];
-    q.hi[w] = c.hi[w];
     q.x[w] = c.lo[w] ^ c.hi[w];
   }
   return q;
 }
 
-// Sum over the 128 elements of |q_e - k_e| for 2-bit codes in bit planes.
-// Per element with a = 2ah + al, b = 2bh + bl:  |a - b| = L + 2A where
-// L = al ^ bl and A = (ah ^ bh) & ~(L & (al ^ ah)). Checked exhaustively over
-// all 16 (a, b) pairs in tests/test_layout.py.
-__device__ __forceinline__ uint32_t l1_distance(const QCode& q, const uint32_t klo[4],
-                                                const uint32_t khi[4]) {
-  uint32_t d = 0;
+// Carry-save adder: a + b + c = s + 2 cy, bitwise.
+__device__ __forceinline__ void csa3(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
+  s = a ^ b ^ c;
+  cy = (a & b) | (c & (a ^ b));
+}
+
+// Sum over the 128 elements of |q_e - k_e| for 2-bit codes, key given as its
+// stored (lo, x = lo ^ hi) planes. Per element with a = 2ah + al, b = 2bh + bl:
+// |a - b| = L + 2A where L = al ^ bl and A = (ah ^ bh) & ~(L & (al ^ ah)), and
+// ah ^ bh = X ^ kx ^ L with X = al ^ ah, kx = bl ^ bh, so A is ONE 3-input
+// LOP3 of (X, kx, L). Checked exhaustively over all 16 (a, b) pairs in
+// tests/test_abi.py. The 4 weight-1 words L and 4 weight-2 words A are folded
+// by carry-save adders into 5 popcounts (balances the ALU and XU pipes; see
+// tools/scan_bench.cu).
+__device__ __forceinline__ uint32_t l1_distance(const QCode& q, const uint32_t klo[4], const uint32_t kx[4]) {
+  uint32_t L[4], A[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
-    const uint32_t L = q.lo[w] ^ klo[w];
-    const uint32_t A = (q.hi[w] ^ khi[w]) & ~(L & q.x[w]);
-    d += __popc(L) + 2u * __popc(A);
+    L[w] = q.lo[w] ^ klo[w];
+    A[w] = (q.x[w] ^ kx[w] ^ L[w]) & ~(L[w] & q.x[w]);
   }
-  return d;
+  uint32_t s1, c1, s2, c2, s3, c3;
+  csa3(L[0], L[1], L[2], s1, c1);                    // weight 1: s1, weight 2: c1
+  const uint32_t s1b = s1 ^ L[3], c1b = s1 & L[3];   // weight 1: s1b, weight 2: c1b
+  csa3(A[0], A[1], A[2], s2, c2);                    // weight 2: s2, weight 4: c2
+  csa3(A[3], c1, c1b, s3, c3);                       // weight 2: s3, weight 4: c3
+  return __popc(s1b) + 2u * (__popc(s2) + __popc(s3)) + 4u * (__popc(c2) + __popc(c3));
 }
 
 // Streaming 128-bit load (no L1 allocation).
@@ -226,6 +238,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Waiting loop with nanosleep back-off, for a thread whose spinning would
+// steal issue slots from compute warps of the same SM sub-partition (the
+// warp arbiter favours the highest warp id, i.e. the producer warp).
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -260,6 +289,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+
+// Programmatic dependent launch (PDL): wait for the predecessor grid's
+// completion + memory visibility / allow the dependent grid to launch.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Per-thread L2 prefetch of one 128-byte line. (The bulk TMA prefetch takes
 // warp-uniform operands, so divergent per-lane use serializes; this does not.)

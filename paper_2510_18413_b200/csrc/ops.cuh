@@ -55,16 +55,16 @@ __device__ __forceinline__ uint32_t ref_byte_from_codes(const uint32_t code[4]) 
   return code[0] | (code[1] << 2) | (code[2] << 4) | (code[3] << 6);
 }
 
-// planes: the kv-head's lo plane base; the hi plane is `cap` records later.
+// planes: the kv-head's lo plane base; the x plane (lo ^ hi) is `cap` records later.
 __device__ __forceinline__ void store_code(uint4* planes, int64_t cap, int64_t t, const Code& c) {
   planes[t] = make_uint4(c.lo[0], c.lo[1], c.lo[2], c.lo[3]);
-  planes[cap + t] = make_uint4(c.hi[0], c.hi[1], c.hi[2], c.hi[3]);
+  planes[cap + t] = make_uint4(c.lo[0] ^ c.hi[0], c.lo[1] ^ c.hi[1], c.lo[2] ^ c.hi[2], c.lo[3] ^ c.hi[3]);
 }
 __device__ __forceinline__ Code load_code(const uint4* planes, int64_t cap, int64_t t) {
   const uint4 a = planes[t], b = planes[cap + t];
   Code c;
   c.lo[0] = a.x; c.lo[1] = a.y; c.lo[2] = a.z; c.lo[3] = a.w;
-  c.hi[0] = b.x; c.hi[1] = b.y; c.hi[2] = b.z; c.hi[3] = b.w;
+  c.hi[0] = a.x ^ b.x; c.hi[1] = a.y ^ b.y; c.hi[2] = a.z ^ b.z; c.hi[3] = a.w ^ b.w;
   return c;
 }
 
@@ -152,16 +152,16 @@ score_kernel(const uint4* __restrict__ codes, int64_t cap, int64_t S, int group,
   __syncthreads();
   const QCode q = make_qcode(qs);
   const uint4* lo_plane = codes + (int64_t)hk * 2 * cap;
-  const uint4* hi_plane = lo_plane + cap;
+  const uint4* x_plane = lo_plane + cap;
   const int64_t t0 = (int64_t)blockIdx.x * kScoreThreads * kScoreTokensPerThread + threadIdx.x;
 #pragma unroll
   for (int i = 0; i < kScoreTokensPerThread; ++i) {
     const int64_t t = t0 + (int64_t)i * kScoreThreads;
     if (t < S) {
-      uint32_t lo[4], hi[4];
+      uint32_t lo[4], x[4];
       ld_plane_nc(lo_plane + t, lo);
-      ld_plane_nc(hi_plane + t, hi);
-      scores[(int64_t)hq * S + t] = (int32_t)l1_distance(q, lo, hi);
+      ld_plane_nc(x_plane + t, x);
+      scores[(int64_t)hq * S + t] = (int32_t)l1_distance(q, lo, x);
     }
   }
 }

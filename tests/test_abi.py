@@ -55,23 +55,43 @@ def test_plane_converters_roundtrip(oracle):
     L.adamas_codes_ref_to_planes(ref.ctypes.data, 257, planes.ctypes.data)
     L.adamas_codes_planes_to_ref(planes.ctypes.data, 257, back.ctypes.data)
     assert np.array_equal(ref, back)
-    # element e: lo/hi planes hold the code's bits at bit e//4 of word e%4
+    # element e: the lo plane holds the code's low bit, the x plane low ^ high,
+    # at bit e//4 of word e%4
     codes = oracle.unpack(ref[5])
     for e in range(128):
         lo = (planes[5, e % 4] >> (e // 4)) & 1
-        hi = (planes[5, 4 + e % 4] >> (e // 4)) & 1
-        assert codes[e] == lo | (hi << 1)
+        x = (planes[5, 4 + e % 4] >> (e // 4)) & 1
+        assert codes[e] == lo | ((lo ^ x) << 1)
 
 
 def test_bitplane_distance_identity_exhaustive():
-    """|a-b| = L + 2A with L = al^bl, A = (ah^bh) & ~(L & (al^ah)) — the
-    per-element identity l1_distance() (csrc/common.cuh) relies on."""
+    """|a-b| = L + 2A with L = al^bl, A = (X ^ kx ^ L) & ~(L & X), X = al^ah,
+    kx = bl^bh — the per-element identity l1_distance() (csrc/common.cuh)
+    relies on (the stored planes are lo and lo^hi)."""
     for a in range(4):
         for b in range(4):
             al, ah, bl, bh = a & 1, a >> 1, b & 1, b >> 1
             Lx = al ^ bl
-            A = (ah ^ bh) & (1 - (Lx & (al ^ ah)))
+            X, kx = al ^ ah, bl ^ bh
+            A = (X ^ kx ^ Lx) & (1 - (Lx & X))
+            assert A == (ah ^ bh) & (1 - (Lx & X))
             assert Lx + 2 * A == abs(a - b), (a, b)
+
+
+def test_carry_save_popcount_fold():
+    """The 5-popcount carry-save fold in l1_distance equals sum popc(L) + 2 sum popc(A)."""
+    rng = np.random.default_rng(3)
+    popc = lambda x: bin(int(x)).count("1")  # noqa: E731
+    for _ in range(3000):
+        L = [int(v) for v in rng.integers(0, 2**32, 4)]
+        A = [int(v) for v in rng.integers(0, 2**32, 4)]
+        csa = lambda a, b, c: (a ^ b ^ c, (a & b) | (c & (a ^ b)))  # noqa: E731
+        s1, c1 = csa(L[0], L[1], L[2])
+        s1b, c1b = s1 ^ L[3], s1 & L[3]
+        s2, c2 = csa(A[0], A[1], A[2])
+        s3, c3 = csa(A[3], c1, c1b)
+        got = popc(s1b) + 2 * (popc(s2) + popc(s3)) + 4 * (popc(c2) + popc(c3))
+        assert got == sum(map(popc, L)) + 2 * sum(map(popc, A))
 
 
 def test_bitplane_distance_matches_oracle_on_words(oracle):
@@ -87,7 +107,8 @@ def test_bitplane_distance_matches_oracle_on_words(oracle):
         d = 0
         for w in range(4):
             Lw = int(pa[w] ^ pb[w])
-            A = int(pa[4 + w] ^ pb[4 + w]) & ~(Lw & int(pa[w] ^ pa[4 + w])) & 0xFFFFFFFF
+            X = int(pa[4 + w])  # query x plane = lo ^ hi
+            A = (X ^ int(pb[4 + w]) ^ Lw) & ~(Lw & X) & 0xFFFFFFFF
             d += bin(Lw).count("1") + 2 * bin(A).count("1")
         assert d == oracle.l1_2bit(a, b)
 

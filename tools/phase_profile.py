@@ -1,7 +1,13 @@
-"""Per-phase timing of the fused decode kernel (globaltimer stamps per CTA).
+"""Per-phase timing of the fused decode kernel in steady state.
 
-    python tools/phase_profile.py [--heads 32 --kv-heads 32 --seq 32768 --budget 128 --cluster 4]
-Prints mean / max over CTAs of each phase's duration (us) for one layer's launch.
+    python tools/phase_profile.py [--heads 32 --kv-heads 32 --seq 32768 --budget 128 --cluster 4 --layers 8]
+
+The last of `layers` back-to-back launches (captured in a CUDA graph, like
+bench.py) is traced. To keep the probe from perturbing what it measures, each
+graph records ONE phase stamp (selected through ADAMAS_DBG bits 8..12) plus the
+CTA start/end globaltimer stamps; the script re-captures once per phase and
+reports, per phase boundary, the mean / max over CTAs of the time since the
+CTA started (globaltimer, ns resolution ~32 ns).
 """
 import argparse
 import ctypes as C
@@ -18,6 +24,7 @@ ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--budget", type=int, default=128)
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--cluster", default="")
+ap.add_argument("--traced", type=int, default=-1, help="index of the traced layer")
 args = ap.parse_args()
 if args.cluster:
     os.environ["ADAMAS_CLUSTER"] = args.cluster
@@ -25,47 +32,72 @@ import paper_2510_18413_b200 as ad  # noqa: E402
 from paper_2510_18413_b200._lib import load  # noqa: E402
 
 L = load()
-g = torch.Generator(device="cuda").manual_seed(0)
+gen = torch.Generator(device="cuda").manual_seed(0)
 caches = []
 for _ in range(args.layers):
     c = ad.KvCache(args.kv_heads, args.seq + 1, torch.bfloat16)
     for s0 in range(0, args.seq - 1, 4096):
         n = min(4096, args.seq - 1 - s0)
-        c.update(torch.randn((n, args.kv_heads, 128), generator=g, device="cuda").bfloat16(),
-                 torch.randn((n, args.kv_heads, 128), generator=g, device="cuda").bfloat16())
+        c.update(torch.randn((n, args.kv_heads, 128), generator=gen, device="cuda").bfloat16(),
+                 torch.randn((n, args.kv_heads, 128), generator=gen, device="cuda").bfloat16())
     caches.append(c)
-q = torch.randn((args.heads, 128), device="cuda").bfloat16()
-k = torch.randn((args.kv_heads, 128), device="cuda").bfloat16()
-trace = torch.zeros(4096 * 16 + 4096 * 16 * 4, dtype=torch.int64, device="cuda")
-names = ["tma+zero", "encode+append", "scan", "hist_exchange", "threshold", "compact_count", "compact_emit",
-         "attend_gather", "attend_combine", "inbox_wait", "merge"]
-for rep in range(3):
-    for c in caches:  # layers back to back, the last one is traced
-        L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if c is caches[-1] else None)
+q = torch.randn((args.heads, 128), generator=gen, device="cuda").bfloat16()
+k = torch.randn((args.kv_heads, 128), generator=gen, device="cuda").bfloat16()
+trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+names = ["start", "prologue (zero, q load, barrier init)", "encode + append", "scan", "hist exchange",
+         "threshold", "compact count+scan", "compact emit", "attend gather", "attend combine+push",
+         "inbox wait", "merge"]
+base_dbg = int(os.environ.get("ADAMAS_DBG", "0")) & 0xff
+
+
+def run_layers():
+    for c in caches:
+        L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if c is caches[args.traced] else None)
         c.decode_step(q, k, k, args.budget)
         c.truncate(args.seq - 1)
+    L.adamas_debug_trace(None)
+
+
+def timed_graph(stamp):
+    os.environ["ADAMAS_DBG"] = str(base_dbg | ((stamp + 1) << 8 if stamp >= 0 else 0))
+    trace.zero_()
+    run_layers()
     torch.cuda.synchronize()
-L.adamas_debug_trace(None)
-wt = trace[4096 * 16:].view(4096, 16, 4).cpu().double()
-t = trace[:4096 * 16].view(-1, 16).cpu()
-n = int((t[:, 0] > 0).sum())
-gt = t[:n, 14:16].double() / 1000.0  # globaltimer ns -> us
-print(f"globaltimer: CTA start spread {(gt[:, 0].max() - gt[:, 0].min()):.2f} us, first start -> last end "
-      f"{(gt[:, 1].max() - gt[:, 0].min()):.2f} us, end spread {(gt[:, 1].max() - gt[:, 1].min()):.2f} us")
-t = t[:n, :14].double()
-GHZ = float(os.environ.get("SM_GHZ", "1.965"))  # clock64 stamps -> us
-t = t / (GHZ * 1000.0)
-print(f"CTAs {n}; per-CTA span mean {(t[:, 11] - t[:, 0]).mean():.2f} us max {(t[:, 11] - t[:, 0]).max():.2f} us")
-if os.environ.get("ADAMAS_DBG", "0") == "8":
-    d = t[:, 5] - t[:, 7]
-    print(f"  [bare barrier after p1: mean {d.mean():.2f} max {d.max():.2f}]")
-if int(os.environ.get("ADAMAS_DBG", "0")) & 16:
-    w = wt[:n] / (GHZ * 1000.0)
-    a = (w[:, :, 1] - w[:, :, 0])
-    b = (w[:, :, 2] - w[:, :, 1])
-    print(f"  [p2 per-warp: cnt-loop mean {a.mean():.3f} max {a.max():.3f}; emit mean {b.mean():.3f} max {b.max():.3f}]")
-    endw = w[:, :, 2]
-    print(f"  [p2 end spread within CTA: mean {(endw.max(1).values - endw.min(1).values).mean():.3f}]")
-for i, nm in enumerate(names):
-    d = (t[:, i + 1] - t[:, i])
-    print(f"{nm:14s} mean {d.mean():7.2f} us  max {d.max():7.2f} us  min {d.min():7.2f}")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run_layers()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    t = trace.view(-1, 16).cpu()
+    n = int((t[:, 14] > 0).sum())
+    t = t[:n].double()
+    if not (base_dbg & 64):  # clock64 stamps -> ns
+        t = t / float(os.environ.get("SM_GHZ", "1.965"))
+    return e0.elapsed_time(e1) * 1000 / len(caches), t
+
+
+us, t = timed_graph(-1)
+span = (t[:, 15] - t[:, 14]) / 1000.0
+print(f"graph: {us:.2f} us per layer; traced launch: {t.shape[0]} CTAs, per-CTA span mean {span.mean():.2f} "
+      f"max {span.max():.2f}" + (f", CTA start spread {(t[:, 14].max() - t[:, 14].min()) / 1000:.2f} us, first start"
+                                 f" -> last end {(t[:, 15].max() - t[:, 14].min()) / 1000:.2f} us"
+                                 if base_dbg & 64 else " (clock64 stamps; ADAMAS_DBG=64 for globaltimer)"))
+prev = torch.zeros(t.shape[0], dtype=torch.float64)
+print(f"{'phase (ends at stamp)':42s} {'cum mean':>9s} {'cum max':>9s} {'delta':>7s}")
+for i in range(1, 12):
+    us_i, ti = timed_graph(i)
+    cum = (ti[:, i] - ti[:, 14]) / 1000.0
+    d = cum.mean() - prev.mean()
+    print(f"{names[i]:42s} {cum.mean():9.2f} {cum.max():9.2f} {d:7.2f}   (graph {us_i:.2f} us/layer)")
+    prev = cum
+for i in (12, 13):
+    us_i, ti = timed_graph(i)
+    cum = (ti[:, i] - ti[:, 14]) / 1000.0
+    print(f"stamp {i} ({'encode start' if i == 12 else 'encode end'}): cum mean {cum.mean():.2f} max {cum.max():.2f}")
+os.environ["ADAMAS_DBG"] = str(base_dbg)
