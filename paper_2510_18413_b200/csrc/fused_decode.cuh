@@ -451,12 +451,26 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     const int eq_budget = max(0, need - pre_eq);  // ... of which this rank may take
     const int out_off = pre_lt + min(pre_eq, need);
     const uint16_t* dg = dist + g * p.chunk;
+    const T* Kg = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
+    const T* Vg = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
     int my_lt = 0, my_eq = 0;
     for (int grp = grp0; grp < grp1; ++grp) {
       uint32_t ltm, eqm;
       group_masks(dg + grp * 32, thr, len - grp * 32, ltm, eqm);
       my_lt += __popc(ltm);
       my_eq += __popc(eqm);
+      // warm L2 for the gather: every row at distance <= T (a superset of the
+      // survivors), one prefetch per 128-B line
+      for (uint32_t m = ltm | eqm; m; m &= m - 1) {
+        const int t = grp * 32 + __ffs(m) - 1;
+        const char* kp = reinterpret_cast<const char*>(Kg + (int64_t)t * kHeadDim);
+        const char* vp = reinterpret_cast<const char*>(Vg + (int64_t)t * kHeadDim);
+#pragma unroll
+        for (int c = 0; c < (int)(kHeadDim * sizeof(T)); c += 128) {
+          prefetch_l2(kp + c);
+          prefetch_l2(vp + c);
+        }
+      }
     }
     int lt_before, eq_before, lt_tot, eq_tot;
     head_scan2<G>(my_lt, my_eq, lt_before, eq_before, lt_tot, eq_tot, scratch);
@@ -513,25 +527,43 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
           const int64_t t = sel[g * selcap + r];
           kb[b] = Raw4<T>::load(Kh + t * kHeadDim);
           vb[b] = Raw4<T>::load(Vh + t * kHeadDim);
+        } else {
+          kb[b] = typename Raw4<T>::V{};
+          vb[b] = typename Raw4<T>::V{};
         }
       }
+      // B dot products reduced together (the butterflies interleave)
+      float sd[B];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        const int r = r0 + b * WG;
-        if (r < ns) {
-          float kf[4], vf[4];
-          Raw4<T>::to_float(kb[b], kf);
-          Raw4<T>::to_float(vb[b], vf);
-          const float s = warp_sum(qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3]);
-          const float mn = fmaxf(m, s);
-          const float corr = exp2f(m - mn);
-          const float pr = exp2f(s - mn);
-          l = l * corr + pr;
+        float kf[4];
+        Raw4<T>::to_float(kb[b], kf);
+        sd[b] = r0 + b * WG < ns ? qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3] : 0.f;
+      }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) o[j] = o[j] * corr + pr * vf[j];
-          m = mn;
+      for (int m2 = 16; m2 > 0; m2 >>= 1)
+#pragma unroll
+        for (int b = 0; b < B; ++b) sd[b] += __shfl_xor_sync(kFull, sd[b], m2);
+      float mx = m;
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (r0 + b * WG < ns) mx = fmaxf(mx, sd[b]);
+      const float corr = exp2f(m - mx);
+      l *= corr;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] *= corr;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (r0 + b * WG < ns) {
+          float vf[4];
+          Raw4<T>::to_float(vb[b], vf);
+          const float pr = exp2f(sd[b] - mx);
+          l += pr;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[j] += pr * vf[j];
         }
       }
+      m = mx;
     }
     ADAMAS_TRACE(8);
     float* wp = wpart + warp * kPartStride;

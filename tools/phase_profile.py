@@ -45,8 +45,8 @@ q = torch.randn((args.heads, 128), generator=gen, device="cuda").bfloat16()
 k = torch.randn((args.kv_heads, 128), generator=gen, device="cuda").bfloat16()
 trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
 names = ["start", "prologue (zero, q load, barrier init)", "encode + append", "scan", "hist exchange",
-         "threshold", "compact count+scan", "compact emit", "attend gather", "attend combine+push",
-         "inbox wait", "merge"]
+         "threshold", "compact count (+L2 prefetch) + scan", "compact emit",
+         "attend gather", "attend combine + push", "inbox wait", "merge"]
 base_dbg = int(os.environ.get("ADAMAS_DBG", "0")) & 0xff
 
 
@@ -99,5 +99,5 @@ for i in range(1, 12):
 for i in (12, 13):
     us_i, ti = timed_graph(i)
     cum = (ti[:, i] - ti[:, 14]) / 1000.0
-    print(f"stamp {i} ({'encode start' if i == 12 else 'encode end'}): cum mean {cum.mean():.2f} max {cum.max():.2f}")
+    print(f"stamp {i}: cum mean {cum.mean():.2f} max {cum.max():.2f}")
 os.environ["ADAMAS_DBG"] = str(base_dbg)
