@@ -299,7 +299,7 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt[0])
-    if not torch.isfinite(hout).all():
+    if not torch.isfinite(hout).all() and not int(os.environ.get("ADAMAS_DBG", "0")):
         raise SystemExit("non-finite attention output")
     h2d = (hq[0].numel() + hk[0].numel() + hv[0].numel()) * es
     d2h = hout[0].numel() * 4

@@ -42,9 +42,10 @@ def load() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
-        raise ImportError(f"{LIB} is not built; run __graft_entry__.build() (no CPU fallback exists)")
-    L = C.CDLL(LIB)
+    lib = os.environ.get("ADAMAS_LIB", LIB)  # A/B experiments may point at another build of the same ABI
+    if not os.path.exists(lib):
+        raise ImportError(f"{lib} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(lib)
     vp, i32, i64, sz = C.c_void_p, C.c_int, C.c_int64, C.c_size_t
     L.adamas_version.restype = C.c_char_p
     L.adamas_last_error.restype = C.c_char_p
@@ -68,7 +69,7 @@ def load() -> C.CDLL:
     L.adamas_debug_trace.argtypes = [vp]
     for name in EXPORTED:
         if not hasattr(L, name):
-            raise ImportError(f"{LIB} does not export {name}")
+            raise ImportError(f"{lib} does not export {name}")
     _lib = L
     return L
 

@@ -130,6 +130,11 @@ int check_heads(const adamas_cache* c, int n_q) {
 }
 
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 // ----------------------------------------------------------------- fused launcher
 template <typename T, int G>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
@@ -147,7 +152,7 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
   cfg.blockDim = dim3(kFusedThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)C;
   attr[0].val.clusterDim.y = 1;
@@ -166,9 +171,9 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
     if ((int64_t)prm.n_seqs * prm.n_kv > max_clusters[C]) prm.pdl = 0;
   }
   if (prm.pdl) {
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.numAttrs = 2;
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
   }
   ADAMAS_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   return ADAMAS_OK;
@@ -185,10 +190,7 @@ int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaSt
   return kFusedUnsupported;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
+
 
 // Chooses the cluster size C (CTAs per (sequence, kv-head) unit) and the
 // per-rank chunk, then launches. Returns kFusedUnsupported when the shape does
@@ -211,8 +213,10 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
     int64_t chunk = (s_max + C - 1) / C;
     chunk = (chunk + 255) / 256 * 256;
     const int selcap = (int)std::min<int64_t>(budget, chunk);
-    // one CTA per SM when the grid fits the machine, else two
-    const size_t smem_cap = (size_t)units * C <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
+    // one CTA per SM when the grid fits the machine, else two (always two
+    // with the 8-warp build, so consecutive launches co-reside)
+    size_t smem_cap = kCtasPerSm == 1 && (size_t)units * C <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
+    if (env_int("ADAMAS_SMEM_KB", 0) > 0) smem_cap = (size_t)env_int("ADAMAS_SMEM_KB", 0) * 1024;  // experiments
     const FusedSmem base(G, C, (int)chunk, selcap, 0);
     const int want = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (chunk + kStageTok - 1) / kStageTok));
     int stages = env_int("ADAMAS_STAGES", 0);
@@ -226,7 +230,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       C *= 2;
       continue;
     }
-    if (L.total <= smem_cap || (stages == 2 && L.total <= 220 * 1024)) {
+    if (L.total <= smem_cap || (stages == 2 && L.total <= (kCtasPerSm == 1 ? 220 : 108) * 1024)) {
       FusedParams prm{};
       prm.n_seqs = n_seqs;
       prm.n_kv = n_kv;

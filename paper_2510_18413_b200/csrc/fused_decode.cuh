@@ -34,7 +34,11 @@
 
 namespace adamas_dev {
 
-constexpr int kConsumerWarps = 16;
+#ifndef ADAMAS_CWARPS
+#define ADAMAS_CWARPS 16  // consumer warps per CTA: 16 (1 CTA/SM) or 8 (2 CTAs/SM)
+#endif
+constexpr int kConsumerWarps = ADAMAS_CWARPS;
+constexpr int kCtasPerSm = kConsumerWarps >= 16 ? 1 : 2;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kProducerWarp = kConsumerWarps;
 constexpr int kFusedThreads = kConsumers + 32;
@@ -46,7 +50,8 @@ constexpr int kMaxG = 8;
 constexpr int kMaxSeqs = 64;
 constexpr int kPartStride = 132;  // floats per partial: m, l, pad, pad, o[128]
 constexpr int kFusedUnsupported = -100;
-constexpr int kTraceTid = 15 * 32;  // diagnostics: the thread that takes phase stamps
+constexpr int kTokPerThread = 1024 / (kConsumerWarps * 32);  // tokens per consumer thread per stage
+constexpr int kTraceTid = (kConsumerWarps - 1) * 32;  // diagnostics: the thread that takes phase stamps
 
 struct FusedSeq {
   uint4* codes;  // this sequence's cache: [n_kv][2 planes][cap] x 16 B
@@ -184,7 +189,7 @@ __device__ __forceinline__ void group_masks(const uint16_t* d32, int thr, int va
 }
 
 template <typename T, int G>
-__global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+__global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   static_assert(G >= 1 && G <= kMaxG && (kConsumerWarps % G) == 0, "G must divide the warp count");
   constexpr int WG = kConsumerWarps / G;  // consumer warps per q-head
   constexpr int NT = kConsumers / G;      // consumer threads per q-head
@@ -342,15 +347,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     const uint4* sx = slo + kStageTok;
     const int base = st * kStageTok;
     const int ntok = min(kStageTok, mem_len - base);
-    uint4 a[2], b[2];
+    uint4 a[kTokPerThread], b[kTokPerThread];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kTokPerThread; ++u) {
       const int j = tid + u * kConsumers;
       if (j < ntok) { a[u] = slo[j]; b[u] = sx[j]; }
     }
-    uint32_t d[2][G];
+    uint32_t d[kTokPerThread][G];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kTokPerThread; ++u) {
       const uint32_t lo[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, x[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
 #pragma unroll
       for (int g = 0; g < G; ++g) d[u][g] = l1_distance(qc[g], lo, x);
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) fused_decode_kernel(const __
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[slot]);  // this warp is done reading the slot
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kTokPerThread; ++u) {
       const int j = tid + u * kConsumers;
       if (j < ntok) {
 #pragma unroll

@@ -1,0 +1,114 @@
+// Cost of the fused kernel's post-scan building blocks in isolation (cycles
+// per execution, 512 consumer threads + 1 idle producer warp, 1 CTA/SM):
+// the compaction count pass (group_masks + head_scan2 + consumer_sync).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2510_18413_b200/csrc -o tools/phase_bench tools/phase_bench.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+
+#include "fused_decode.cuh"
+
+using namespace adamas_dev;
+
+template <int MODE>
+__global__ void __launch_bounds__(kFusedThreads, 1) probe(const uint16_t* src, int iters, int thr, long long* cyc,
+                                                          int* sink) {
+  __shared__ __align__(16) uint16_t dist[8192];
+  __shared__ int scratch[2 * kConsumerWarps];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) dist[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x >= kConsumers) return;
+  const int tid = threadIdx.x;
+  const int len = 8192, ngroups = 256, gpt = 1;
+  const int grp0 = min(ngroups, tid * gpt), grp1 = min(ngroups, grp0 + gpt);
+  int acc = 0;
+  consumer_sync();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    int a = 0, b = 0;
+    if (MODE & 1) {
+      for (int grp = grp0; grp < grp1; ++grp) {
+        uint32_t ltm, eqm;
+        group_masks(dist + grp * 32, thr + (it & 1), len - grp * 32, ltm, eqm);
+        a += __popc(ltm);
+        b += __popc(eqm);
+      }
+    }
+    if (MODE & 8) {  // ballot formulation: warp w owns groups [16 w, 16 w + 16), lane j keeps group j
+      const int lane = tid & 31, warp = tid >> 5;
+      const int T = thr + (it & 1);
+      uint32_t mlt = 0, meq = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int d = dist[(warp * 16 + j) * 32 + lane];
+        const uint32_t bl = __ballot_sync(kFull, d < T), be = __ballot_sync(kFull, d == T);
+        if (lane == j) { mlt = bl; meq = be; }
+      }
+      a = __popc(mlt);
+      b = __popc(meq);
+    }
+    if (MODE & 16) {  // cooperative hot blocks: thread owns 16 tokens; hot blocks processed by the warp
+      const int lane = tid & 31;
+      const int T = thr + (it & 1);
+      const int t0 = tid * 16;
+      const uint32_t kle = ((uint32_t)T * 0x00010001u) | 0x80008000u;
+      const uint4 a0 = *reinterpret_cast<const uint4*>(dist + t0);
+      const uint4 a1 = *reinterpret_cast<const uint4*>(dist + t0 + 8);
+      const uint32_t x = (kle - a0.x) | (kle - a0.y) | (kle - a0.z) | (kle - a0.w) | (kle - a1.x) | (kle - a1.y) |
+                         (kle - a1.z) | (kle - a1.w);
+      const bool any = (x & 0x80008000u) != 0u;
+      uint32_t ml = 0, me = 0;
+      for (uint32_t hot = __ballot_sync(kFull, any); hot; hot &= hot - 1) {
+        const int h = __ffs(hot) - 1;
+        const int t0h = __shfl_sync(kFull, t0, h);
+        const int d = lane < 16 ? (int)dist[t0h + lane] : 0x7fff;
+        const uint32_t bl = __ballot_sync(kFull, d < T), be = __ballot_sync(kFull, d == T);
+        if (lane == h) { ml = bl; me = be; }
+      }
+      a = __popc(ml);
+      b = __popc(me);
+    }
+    int x0 = a, x1 = b, x2 = 0, x3 = 0;
+    if (MODE & 2) head_scan2<1>(a, b, x0, x1, x2, x3, scratch);
+    if (MODE & 4) consumer_sync();
+    acc += x0 + x1 + x2 + x3;
+  }
+  const long long t1 = clock64();
+  if (tid == 0) cyc[blockIdx.x] = t1 - t0;
+  if (acc == 123456789) sink[0] = acc;
+}
+
+template <int MODE>
+void run(const char* name, const uint16_t* src, long long* cyc, int* sink) {
+  const int iters = 200;
+  for (int r = 0; r < 2; ++r) probe<MODE><<<128, kFusedThreads>>>(src, iters, 131, cyc, sink);
+  cudaDeviceSynchronize();
+  long long h[128];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  double m = 0;
+  for (int i = 0; i < 128; ++i) m += h[i] / 128.0;
+  printf("%-44s %8.0f cycles per pass (%.3f us)  [%s]\n", name, m / iters, m / iters / 1965.0,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  uint16_t h[8192];
+  unsigned z = 12345;
+  // distances ~ N(160, 11) (random 2-bit codes at d = 128); thr = the 0.4% quantile
+  for (int i = 0; i < 8192; ++i) {
+    int acc = 0;
+    for (int k = 0; k < 12; ++k) { z = z * 1664525u + 1013904223u; acc += (z >> 16) & 0xff; }
+    h[i] = (uint16_t)(160 + (acc - 12 * 127.5) * 11.0 / 256.0);
+  }
+  uint16_t* src; long long* cyc; int* sink;
+  cudaMalloc(&src, sizeof(h)); cudaMalloc(&cyc, 128 * 8); cudaMalloc(&sink, 64);
+  cudaMemcpy(src, h, sizeof(h), cudaMemcpyHostToDevice);
+  run<4>("consumer_sync only", src, cyc, sink);
+  run<1 | 4>("group_masks + sync", src, cyc, sink);
+  run<2 | 4>("head_scan2 + sync", src, cyc, sink);
+  run<1 | 2 | 4>("group_masks + head_scan2 + sync", src, cyc, sink);
+  run<8 | 4>("ballot masks + sync", src, cyc, sink);
+  run<8 | 2 | 4>("ballot masks + head_scan2 + sync", src, cyc, sink);
+  run<16 | 4>("cooperative hot blocks + sync", src, cyc, sink);
+  run<16 | 2 | 4>("cooperative hot blocks + head_scan2 + sync", src, cyc, sink);
+  return 0;
+}
