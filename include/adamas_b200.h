@@ -138,6 +138,39 @@ int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const vo
                                const void* k_new, const void* v_new, int64_t budget, float* out,
                                int32_t* idx, void* stream);
 
+/* ---------------------------------------------------------------- sequence-sharded decode
+ * One decode step over a sequence split in contiguous token ranges across
+ * ranks (the reference's single score_all + top_k +
+ * sparse_attention, estimator.cpp:45-90 and attention.cpp:8-45, over the whole
+ * sequence). Per rank: local candidates -> all-gather the keys -> select and
+ * attend -> all-gather the partials -> LSE merge. Bit-exact selection: a
+ * member of the global (distance, index) top-k has fewer than k predecessors
+ * in its own range, so it is among that range's candidates.
+ *
+ * Local candidates: optionally appends (k_new, v_new) with its code (the rank
+ * owning the sequence tail), encodes q, scans the local cache and writes this
+ * range's top-`budget` keys per q-head, cand_keys uint32 [n_q][budget]:
+ * (distance << 23) | (base_index + local token); unused entries 0xFFFFFFFF.
+ * Global indices must stay below 2^23. */
+int adamas_seq_local_candidates(adamas_cache* cache, const void* q, int n_q_heads, const void* k_new,
+                                const void* v_new, int append, int64_t base_index, int64_t budget,
+                                uint32_t* cand_keys, void* stream);
+
+/* Select + attend: gathered uint32 [n_ranks][n_q][budget] keys of every rank,
+ * total_len = tokens of the whole sequence (after this step's append),
+ * rank_base = global index of this cache's token 0. Writes the partial of this
+ * rank's survivors, float32 [n_q][132] = (m in natural-log units, l, 0, 0,
+ * o[128] unnormalised), and optionally the global selection int32
+ * [n_q][budget] ascending (-1 past min(budget, total_len)).
+ * n_ranks * budget <= 8192, budget <= 2048. */
+int adamas_seq_select_attend(const adamas_cache* cache, const void* q, int n_q_heads, const uint32_t* gathered,
+                             int n_ranks, int64_t budget, int64_t total_len, int64_t rank_base, float* partial,
+                             int32_t* global_idx, void* stream);
+
+/* Log-sum-exp merge of the ranks' partials float32 [n_ranks][n_q][132] into
+ * out float32 [n_q][128]. */
+int adamas_lse_merge(const float* partials, int n_ranks, int n_q_heads, float* out, void* stream);
+
 /* ---------------------------------------------------------------- diagnostics
  * Subsequent fused decode launches write up to 16 %globaltimer stamps per CTA
  * (phase boundaries) into device_buffer[blockIdx * 16 + i]; NULL disables. */

@@ -23,7 +23,8 @@ EXPORTED = [
     "adamas_cache_append", "adamas_cache_append_coded", "adamas_cache_codes_ref",
     "adamas_encode_query", "adamas_score", "adamas_topk", "adamas_sparse_attention",
     "adamas_decode_step", "adamas_decode_step_batched", "adamas_codes_ref_to_planes",
-    "adamas_codes_planes_to_ref", "adamas_debug_trace",
+    "adamas_codes_planes_to_ref", "adamas_debug_trace", "adamas_seq_local_candidates",
+    "adamas_seq_select_attend", "adamas_lse_merge",
 ]
 
 
@@ -67,6 +68,9 @@ def load() -> C.CDLL:
     L.adamas_codes_ref_to_planes.argtypes = [vp, i64, vp]
     L.adamas_codes_planes_to_ref.argtypes = [vp, i64, vp]
     L.adamas_debug_trace.argtypes = [vp]
+    L.adamas_seq_local_candidates.argtypes = [vp, vp, i32, vp, vp, i32, i64, i64, vp, vp]
+    L.adamas_seq_select_attend.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, vp, vp, vp]
+    L.adamas_lse_merge.argtypes = [vp, i32, i32, vp, vp]
     for name in EXPORTED:
         if not hasattr(L, name):
             raise ImportError(f"{lib} does not export {name}")

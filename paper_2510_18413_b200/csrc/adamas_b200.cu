@@ -197,12 +197,13 @@ int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaSt
 // not fit the single-launch kernel (the caller composes operators instead).
 int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n_q, int dtype, const void* q,
                         const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
-                        cudaStream_t s) {
+                        cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0) {
   const int G = n_q / n_kv;
   if (G != 1 && G != 2 && G != 4 && G != 8) return kFusedUnsupported;
   if (n_seqs > kMaxSeqs || budget > (1 << 20)) return kFusedUnsupported;
   int64_t s_max = 0;
-  for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + 1);
+  for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + append);
+  if (s_max < 1) s_max = 1;
   const int units = n_seqs * n_kv;
   int C = env_int("ADAMAS_CLUSTER", 0);
   if (C <= 0) {
@@ -241,6 +242,9 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       prm.exact_encode = env_int("ADAMAS_EXACT_ENCODE", 0);
       prm.dbg = env_int("ADAMAS_DBG", 0);
       prm.pdl = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
+      prm.append = append;
+      prm.cand = cand;
+      prm.cand_base = cand_base;
       prm.q = q;
       prm.k_new = k_new;
       prm.v_new = v_new;
@@ -487,6 +491,60 @@ int adamas_decode_step(adamas_cache* c, const void* q, int n_q, const void* k_ne
                        int64_t budget, float* out, int32_t* idx, void* stream) {
   adamas_cache* arr[1] = {c};
   return adamas_decode_step_batched(arr, 1, q, n_q, k_new, v_new, budget, out, idx, stream);
+}
+
+int adamas_seq_local_candidates(adamas_cache* c, const void* q, int n_q, const void* k_new, const void* v_new,
+                                int append, int64_t base_index, int64_t budget, uint32_t* cand_keys, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (budget < 1) return fail(ADAMAS_ERR_CONFIG, "seq_local_candidates: budget must be >= 1");
+  if (!q || !cand_keys || (append && (!k_new || !v_new))) return fail(ADAMAS_ERR_CONFIG, "seq_local_candidates: null pointer");
+  if (base_index < 0 || base_index + c->seq_len + (append ? 1 : 0) > (int64_t(1) << 23))
+    return fail(ADAMAS_ERR_CONFIG, "seq_local_candidates: global token index must stay below 2^23");
+  if (append && c->seq_len + 1 > c->capacity) return fail(ADAMAS_ERR_CONFIG, "seq_local_candidates: cache capacity exceeded");
+  if (c->seq_len + (append ? 1 : 0) == 0) {  // empty shard: no candidates
+    ADAMAS_CUDA(cudaMemsetAsync(cand_keys, 0xff, (size_t)n_q * budget * sizeof(uint32_t), as_stream(stream)));
+    return ADAMAS_OK;
+  }
+  adamas_cache* arr[1] = {c};
+  const int rc = fused_decode_launch(arr, 1, c->n_kv, n_q, c->dtype, q, k_new, v_new, budget, nullptr, nullptr,
+                                     as_stream(stream), append ? 1 : 0, cand_keys, base_index);
+  if (rc == kFusedUnsupported) return fail(ADAMAS_ERR_CONFIG, "seq_local_candidates: shape not supported by the fused kernel");
+  if (rc != ADAMAS_OK) return rc;
+  if (append) {
+    c->dirty_from = c->seq_len;
+    c->seq_len += 1;
+  }
+  return ADAMAS_OK;
+}
+
+int adamas_seq_select_attend(const adamas_cache* c, const void* q, int n_q, const uint32_t* gathered, int n_ranks,
+                             int64_t budget, int64_t total_len, int64_t rank_base, float* partial, int32_t* global_idx,
+                             void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (n_ranks < 1 || budget < 1 || total_len < 1) return fail(ADAMAS_ERR_CONFIG, "seq_select_attend: bad sizes");
+  if ((int64_t)n_ranks * budget > kSelMaxKeys || budget > kSelMaxSurv)
+    return fail(ADAMAS_ERR_CONFIG, "seq_select_attend: n_ranks * budget exceeds 8192 (or budget > 2048)");
+  if (!q || !gathered || !partial) return fail(ADAMAS_ERR_CONFIG, "seq_select_attend: null pointer");
+  const int k_eff = (int)std::min<int64_t>(budget, total_len);
+  const int group = n_q / c->n_kv;
+  if (c->dtype == ADAMAS_BF16)
+    seq_select_attend_kernel<__nv_bfloat16><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
+        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, gathered,
+        n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx);
+  else
+    seq_select_attend_kernel<float><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
+        (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, gathered, n_ranks, n_q, budget,
+        k_eff, rank_base, c->seq_len, partial, global_idx);
+  return launch_check("seq_select_attend_kernel");
+}
+
+int adamas_lse_merge(const float* partials, int n_ranks, int n_q, float* out, void* stream) {
+  if (n_ranks < 1 || n_q < 1) return fail(ADAMAS_ERR_CONFIG, "lse_merge: bad sizes");
+  if (!partials || !out) return fail(ADAMAS_ERR_CONFIG, "lse_merge: null pointer");
+  lse_merge_kernel<<<n_q, 32, 0, as_stream(stream)>>>(partials, n_ranks, n_q, out);
+  return launch_check("lse_merge_kernel");
 }
 
 void adamas_codes_ref_to_planes(const uint16_t* ref, int64_t n, uint32_t* planes) {

@@ -67,6 +67,9 @@ struct FusedParams {
   int exact_encode;  // 1: always the sequential fp64 sum (diagnostics / tests)
   int dbg;           // diagnostics only: bit1 no idx stores
   int pdl;           // launched with programmatic stream serialization
+  int append;        // 1: append (k_new, v_new) first (decode step); 0: the cache as is
+  uint32_t* cand;    // candidates mode: [n_seqs][n_q][budget] keys (dist << 23 | base + token), no attention
+  int64_t cand_base; // global index of this cache's token 0 (sequence-sharded caches)
   const void* q;      // [n_seqs][n_q][128]
   const void* k_new;  // [n_seqs][n_kv][128]
   const void* v_new;
@@ -206,12 +209,12 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 
   const int64_t cap = p.seq[si].cap;
   const int64_t s_old = p.seq[si].s_old;
-  const int64_t S = s_old + 1;
+  const int64_t S = s_old + (p.append ? 1 : 0);
   const int64_t start = (int64_t)rank * p.chunk;
   const int64_t end = min(S, start + (int64_t)p.chunk);
   const int len = end > start ? (int)(end - start) : 0;
   const int mem_len = (int)max((int64_t)0, min(end, s_old) - start);  // already in HBM
-  const bool has_new = (s_old >= start) && (s_old < end);
+  const bool has_new = p.append && (s_old >= start) && (s_old < end);
   const int selcap = min(p.budget, p.chunk);
   const int ring = p.stages;
 
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
     // C partials per q-head it merges
     mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
-    if (n_owned) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
+    if (n_owned && !p.cand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
   }
   // the G query heads (and the new key) are loaded before the barrier so the
   // global-load latency overlaps the barrier initialisation
@@ -498,6 +501,9 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
           const int tok = (int)start + grp * 32 + i;
           if (pos < selcap) sel[g * selcap + pos] = tok;
           if (idx_row) idx_row[pos] = tok;
+          if (p.cand)  // (distance, global index) key: the distributed top-k's order
+            p.cand[((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off + pos] =
+                ((uint32_t)dg[grp * 32 + i] << 23) | (uint32_t)(p.cand_base + tok);
           ++pos;
         }
       }
@@ -506,9 +512,14 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       int32_t* row = p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
     }
+    if (rank == 0 && p.cand && t_in == 0) {
+      uint32_t* row = p.cand + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget;
+      for (int i = k_eff; i < p.budget; ++i) row[i] = 0xffffffffu;
+    }
   }
   consumer_sync();
   ADAMAS_TRACE(7);
+  if (p.cand) return;  // candidates mode: the selection is the product
 
   // ---------------------------------------------------------------- attend
   {

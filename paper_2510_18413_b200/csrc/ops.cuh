@@ -334,3 +334,196 @@ attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int
 }
 
 }  // namespace adamas_dev
+
+namespace adamas_dev {
+
+// ----------------------------------------------------------------- sequence-sharded decode
+// Distributed top-k. Every rank holds a contiguous token range
+// of the sequence and contributes its local top-k keys (dist << 23 | global
+// index, the (score, index) order of top_k, estimator.cpp:75-90). A member of
+// the global top-k has fewer than k predecessors in its own shard, so it is
+// among that shard's keys: the selection rebuilt from the gathered keys is
+// exactly the single-device one. One CTA per q-head rebuilds it, attends over
+// this rank's survivors (rows of the local cache) and emits the partial
+// (m, l, o[128]) for the log-sum-exp merge (attention.cpp:8-38 semantics).
+constexpr int kSelThreads = 512;
+constexpr int kSelMaxKeys = 8192;   // n_ranks * budget per q-head
+constexpr int kSelMaxSurv = 2048;   // budget
+constexpr int kSelBins = 512;
+constexpr int kPartialStride = 132;  // m (natural-log units), l, pad, pad, o[128]
+
+__device__ __forceinline__ void sel_block_excl_scan(int v, int& excl, int& total, int* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const int o = __shfl_up_sync(kFull, incl, m);
+    if (lane >= m) incl += o;
+  }
+  if (lane == 31) scratch[warp] = incl;
+  __syncthreads();
+  int before = 0, sum = 0;
+  for (int w = 0; w < kSelThreads / 32; ++w) {
+    const int x = scratch[w];
+    before += w < warp ? x : 0;
+    sum += x;
+  }
+  excl = before + incl - v;
+  total = sum;
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSelThreads)
+seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
+                         const T* __restrict__ q, const uint32_t* __restrict__ keys, int n_ranks, int n_q,
+                         int64_t budget, int k_eff, int64_t rank_base, int64_t rank_len, float* __restrict__ partial,
+                         int32_t* __restrict__ gidx) {
+  __shared__ int hist[kSelBins];
+  __shared__ int scratch[32];
+  __shared__ int s_T, s_below, n_ties, n_surv, n_local;
+  __shared__ int ties[kSelMaxKeys / 4];
+  __shared__ int surv[kSelMaxSurv];
+  __shared__ int local_rows[kSelMaxSurv];
+  __shared__ float wm[kSelThreads / 32], wl[kSelThreads / 32];
+  __shared__ float wo[kSelThreads / 32][kHeadDim];
+  const int h = blockIdx.x, hk = h / group;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = n_ranks * (int)budget;
+  auto key_at = [&](int j) {  // j = r * budget + i
+    const int r = j / (int)budget, i = j - r * (int)budget;
+    return keys[((int64_t)r * n_q + h) * budget + i];
+  };
+  for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
+  if (tid == 0) { n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0; }
+  __syncthreads();
+  for (int j = tid; j < n; j += kSelThreads) {
+    const uint32_t key = key_at(j);
+    if (key != 0xffffffffu) atomicAdd(&hist[key >> 23], 1);
+  }
+  __syncthreads();
+  {  // T = smallest distance whose cumulative count reaches k_eff (one bin per thread)
+    const int v = hist[tid];
+    int excl, total;
+    sel_block_excl_scan(v, excl, total, scratch);
+    if (excl < k_eff && excl + v >= k_eff) { s_T = tid; s_below = excl; }
+  }
+  __syncthreads();
+  const int Tthr = s_T, need = k_eff - s_below;
+  for (int j = tid; j < n; j += kSelThreads) {
+    const uint32_t key = key_at(j);
+    if (key != 0xffffffffu && (int)(key >> 23) == Tthr) {
+      const int t = atomicAdd(&n_ties, 1);
+      if (t < kSelMaxKeys / 4) ties[t] = (int)(key & 0x7fffffu);
+    }
+  }
+  __syncthreads();
+  const int nt = min(n_ties, kSelMaxKeys / 4);
+  for (int j = tid; j < n; j += kSelThreads) {
+    const uint32_t key = key_at(j);
+    if (key == 0xffffffffu) continue;
+    const int d = (int)(key >> 23), idx = (int)(key & 0x7fffffu);
+    bool take = d < Tthr;
+    if (d == Tthr) {  // ties resolve toward lower indices
+      int r = 0;
+      if (n_ties <= kSelMaxKeys / 4) {
+        for (int t = 0; t < nt; ++t) r += ties[t] < idx;
+      } else {  // more ties than the list holds: rank against every key
+        for (int j2 = 0; j2 < n; ++j2) {
+          const uint32_t k2 = key_at(j2);
+          r += k2 != 0xffffffffu && (int)(k2 >> 23) == Tthr && (int)(k2 & 0x7fffffu) < idx;
+        }
+      }
+      take = r < need;
+    }
+    if (!take) continue;
+    const int s = atomicAdd(&n_surv, 1);
+    if (s < kSelMaxSurv) surv[s] = idx;
+    if (idx >= rank_base && idx < rank_base + rank_len) {
+      const int l = atomicAdd(&n_local, 1);
+      if (l < kSelMaxSurv) local_rows[l] = idx - (int)rank_base;
+    }
+  }
+  __syncthreads();
+  const int ns = min(n_surv, kSelMaxSurv), nl = min(n_local, kSelMaxSurv);
+  if (gidx != nullptr) {  // the global selection, ascending (top_k's output order)
+    for (int i = tid; i < ns; i += kSelThreads) {
+      const int idx = surv[i];
+      int r = 0;
+      for (int j = 0; j < ns; ++j) r += surv[j] < idx;
+      gidx[(int64_t)h * budget + r] = idx;
+    }
+    for (int i = ns + tid; i < budget; i += kSelThreads) gidx[(int64_t)h * budget + i] = -1;
+  }
+  // attention over this rank's survivors: per-warp online softmax, log2 units
+  float qf[4];
+  Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)h * kHeadDim + lane * 4), qf);
+  const float scale = 0.088388347648318440f * kLog2e;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) qf[j] *= scale;
+  const T* Kh = K + (int64_t)hk * cap * kHeadDim + lane * 4;
+  const T* Vh = V + (int64_t)hk * cap * kHeadDim + lane * 4;
+  float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int r = warp; r < nl; r += kSelThreads / 32) {
+    const int64_t t = local_rows[r];
+    float kf[4], vf[4];
+    Raw4<T>::to_float(Raw4<T>::load(Kh + t * kHeadDim), kf);
+    Raw4<T>::to_float(Raw4<T>::load(Vh + t * kHeadDim), vf);
+    const float sd = warp_sum(qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3]);
+    const float mn = fmaxf(m, sd);
+    const float corr = exp2f(m - mn), pr = exp2f(sd - mn);
+    l = l * corr + pr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = o[j] * corr + pr * vf[j];
+    m = mn;
+  }
+  if (lane == 0) { wm[warp] = m; wl[warp] = l; }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) wo[warp][lane * 4 + j] = o[j];
+  __syncthreads();
+  if (warp == 0) {
+    float M = -INFINITY;
+    for (int w = 0; w < kSelThreads / 32; ++w)
+      if (wl[w] > 0.f) M = fmaxf(M, wm[w]);
+    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int w = 0; w < kSelThreads / 32; ++w) {
+      if (!(wl[w] > 0.f)) continue;
+      const float c = exp2f(wm[w] - M);
+      L += wl[w] * c;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += wo[w][lane * 4 + j] * c;
+    }
+    float* pp = partial + (int64_t)h * kPartialStride;
+    if (lane == 0) {
+      pp[0] = L > 0.f ? M / kLog2e : -INFINITY;  // natural-log units
+      pp[1] = L;
+      pp[2] = 0.f;
+      pp[3] = 0.f;
+    }
+    *reinterpret_cast<float4*>(pp + 4 + lane * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
+// out[h] = sum_r e^{m_r - M} o_r / sum_r e^{m_r - M} l_r over the ranks' partials.
+__global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks, int n_q, float* __restrict__ out) {
+  const int h = blockIdx.x, lane = threadIdx.x;
+  float M = -INFINITY;
+  for (int r = 0; r < n_ranks; ++r) {
+    const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
+    if (pp[1] > 0.f) M = fmaxf(M, pp[0]);
+  }
+  float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int r = 0; r < n_ranks; ++r) {
+    const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
+    if (!(pp[1] > 0.f)) continue;
+    const float c = __expf(pp[0] - M);
+    L += pp[1] * c;
+    const float4 v = *reinterpret_cast<const float4*>(pp + 4 + lane * 4);
+    acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  *reinterpret_cast<float4*>(out + (int64_t)h * kHeadDim + lane * 4) =
+      make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+}
+
+}  // namespace adamas_dev
