@@ -30,6 +30,23 @@ sys.path.insert(0, ROOT)
 METRIC = "decode self-attn µs/token/layer @32K, budget 128; code-scan HBM GB/s vs peak"
 UNIT = "us/token/layer"
 
+# BASELINE.json configs (shapes per step; "seqs" = independent requests)
+CONFIGS = {
+    "longchat": dict(heads=32, kv_heads=32, seq=32768, budget=128, layers=32, seqs=1),
+    "llama128k": dict(heads=32, kv_heads=8, seq=131072, budget=128, layers=16, seqs=1),
+    "batched16": dict(heads=32, kv_heads=8, seq=32768, budget=128, layers=4, seqs=16),
+    "seqshard1m": dict(heads=32, kv_heads=8, seq=1048576 // 8, budget=128, layers=16, seqs=1),
+}
+WORKLOAD = {
+    "longchat": "LongChat-7B attention decode: {heads} heads ({kv_heads} kv) x 128, S={seq}, batch 1, budget {budget}",
+    "llama128k": "Llama-3.1-8B GQA attention decode: {heads} q / {kv_heads} kv heads x 128, S={seq}, batch 1, "
+                 "budget {budget}",
+    "batched16": "batched decode: {seqs} requests x S={seq}, Llama-3.1-8B shape ({heads} q / {kv_heads} kv), "
+                 "per-request top-{budget}",
+    "seqshard1m": "1M-token context, {heads} q / {kv_heads} kv heads, one rank's share of an 8-way sequence split "
+                  "(S={seq} per rank): local candidates + distributed select/attend + LSE merge, budget {budget}",
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -37,15 +54,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--heads", type=int, default=32)
-    ap.add_argument("--kv-heads", type=int, default=32)
-    ap.add_argument("--seq", type=int, default=32768)
-    ap.add_argument("--budget", type=int, default=128)
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--config", default="longchat", choices=sorted(CONFIGS),
+                    help="BASELINE.json config: longchat (configs[1], the headline), llama128k (configs[2]), "
+                         "batched16 (configs[3]), seqshard1m (configs[4], per-rank work of the 8-way split)")
+    ap.add_argument("--heads", type=int, default=None)
+    ap.add_argument("--kv-heads", type=int, default=None)
+    ap.add_argument("--seq", type=int, default=None)
+    ap.add_argument("--budget", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--seqs", type=int, default=None, help="independent sequences (requests) per step")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=11)
-    return ap.parse_args()
+    a = ap.parse_args()
+    for k, v in CONFIGS[a.config].items():
+        if getattr(a, k) is None:
+            setattr(a, k, v)
+    return a
 
 
 def load_peaks():
@@ -169,6 +194,54 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+def _prefill(ad, torch, n_kv, S, dtype, gen, cap_extra=1):
+    """A cache with S tokens (bulk encode-append, 4096 tokens per launch)."""
+    c = ad.KvCache(n_kv, S + cap_extra, dtype)
+    done = 0
+    while done < S:
+        n = min(4096, S - done)
+        k = torch.randn((n, n_kv, 128), generator=gen, device="cuda").to(dtype)
+        v = torch.randn((n, n_kv, 128), generator=gen, device="cuda").to(dtype)
+        c.update(k, v)
+        done += n
+    return c
+
+
+def _timed_graph(torch, dist, ws, body, steps, local, sample_clocks=False):
+    """Capture `steps` calls of body(s, stream) in one CUDA graph, warm replay,
+    then time one replay with CUDA events on the capture stream (max over
+    ranks). Returns (elapsed_ms, clock summary or None)."""
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        st = torch.cuda.current_stream()
+        for s in range(steps):
+            body(s, st)
+    graph.replay()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local) if sample_clocks else None
+    if clk:
+        clk.__enter__()
+    e0.record(stream)
+    graph.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt[0])
+        dist.barrier()
+    del graph
+    return ms, (clk.summary() if clk else None)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -179,139 +252,127 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.heads % ws or args.kv_heads % ws:
+    seqshard = args.config == "seqshard1m"
+    if not seqshard and (args.heads % ws or args.kv_heads % ws):
         raise SystemExit("heads must divide across ranks")
-    n_q, n_kv = args.heads // ws, args.kv_heads // ws
+    n_q, n_kv = (args.heads, args.kv_heads) if seqshard else (args.heads // ws, args.kv_heads // ws)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     es = 2 if dtype == torch.bfloat16 else 4
-    S, L, B = args.seq, args.layers, args.budget
+    S, L, B, NS = args.seq, args.layers, args.budget, args.seqs
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1234 + rank)
 
-    # prefill S-1 tokens per layer (bulk encode-append); the timed step appends token S
-    caches = []
-    chunk = 4096
-    for _ in range(L):
-        c = ad.KvCache(n_kv, S + 1, dtype)
-        done = 0
-        while done < S - 1:
-            n = min(chunk, S - 1 - done)
-            k = torch.randn((n, n_kv, 128), generator=gen, device="cuda").to(dtype)
-            v = torch.randn((n, n_kv, 128), generator=gen, device="cuda").to(dtype)
-            c.update(k, v)
-            done += n
-        caches.append(c)
+    # prefill S-1 tokens per (layer, sequence); the timed step appends token S
+    caches = [[_prefill(ad, torch, n_kv, S - 1, dtype, gen) for _ in range(NS)] for _ in range(L)]
     torch.cuda.synchronize()
-    for c in caches:
-        c.raise_on_degenerate()
+    for row in caches:
+        for c in row:
+            c.raise_on_degenerate()
 
     total_steps = args.warmup + args.steps
-    qs = torch.randn((total_steps, L, n_q, 128), generator=gen, device="cuda").to(dtype)
-    ks = torch.randn((total_steps, L, n_kv, 128), generator=gen, device="cuda").to(dtype)
-    vs = torch.randn((total_steps, L, n_kv, 128), generator=gen, device="cuda").to(dtype)
-    out = torch.empty((L, n_q, 128), dtype=torch.float32, device="cuda")
-    idx = torch.empty((L, n_q, B), dtype=torch.int32, device="cuda")
-    stream = torch.cuda.current_stream()
+    qs = torch.randn((total_steps, L, NS, n_q, 128), generator=gen, device="cuda").to(dtype)
+    ks = torch.randn((total_steps, L, NS, n_kv, 128), generator=gen, device="cuda").to(dtype)
+    vs = torch.randn((total_steps, L, NS, n_kv, 128), generator=gen, device="cuda").to(dtype)
+    out = torch.empty((L, NS, n_q, 128), dtype=torch.float32, device="cuda")
+    idx = torch.empty((L, NS, n_q, B), dtype=torch.int32, device="cuda")
 
-    def step(s, ev=None):
-        for l in range(L):
-            if ev is not None:
-                ev[l][0].record(stream)
-            caches[l].decode_step(qs[s, l], ks[s, l], vs[s, l], B, out=out[l], idx=idx[l], stream=stream)
-            if ev is not None:
-                ev[l][1].record(stream)
-        for c in caches:  # keep S fixed: the next step re-appends at position S-1
-            c.truncate(S - 1)
+    if seqshard:
+        # one rank's share of the 8-way split: ranks r < 8 own [r S, (r + 1) S);
+        # this process is rank `rank` of the world, the other shards' keys come
+        # from the all-gather (N > 1) or are synthesized from this shard's keys
+        # with shifted indices (N = 1, the per-GPU work of the 8-GPU job).
+        from paper_2510_18413_b200.seqshard import CudaSeqOps, torch_allgather
+        ops = CudaSeqOps()
+        n_virtual = 8
+        gather = torch_allgather() if ws > 1 else None
+        keys_all = torch.empty((L, n_virtual, n_q, B), dtype=torch.int32, device="cuda")
+        parts_all = torch.empty((L, n_virtual, n_q, 132), dtype=torch.float32, device="cuda")
+        my_slot = rank % n_virtual
+        base = my_slot * S
 
+        def step(s, st):
+            for l in range(L):
+                c = caches[l][0]
+                keys = ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], my_slot == n_virtual - 1,
+                                            base, B, stream=st)
+                if gather is not None:
+                    keys_all[l, :ws].copy_(gather(keys))
+                else:  # other shards: same distances, indices moved to their ranges
+                    for r in range(n_virtual):
+                        keys_all[l, r].copy_(keys + (r - my_slot) * S)
+                part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
+                if gather is not None:
+                    parts_all[l, :ws].copy_(gather(part))
+                else:
+                    parts_all[l].copy_(part.expand(n_virtual, -1, -1))
+                out[l, 0].copy_(ops.lse_merge(parts_all[l], stream=st))
+                if my_slot == n_virtual - 1:
+                    c.truncate(S - 1)
+    else:
+        def step(s, st):
+            for l in range(L):
+                if NS == 1:
+                    caches[l][0].decode_step(qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], B, out=out[l, 0],
+                                             idx=idx[l, 0], stream=st)
+                else:
+                    ad.decode_step_batched(caches[l], qs[s, l], ks[s, l], vs[s, l], B, out=out[l], idx=idx[l],
+                                           stream=st)
+            for row in caches:  # keep S fixed: the next step re-appends at position S-1
+                for c in row:
+                    c.truncate(S - 1)
+
+    stream0 = torch.cuda.current_stream()
     for s in range(args.warmup):  # eager warm-up (also configures the kernels)
-        step(s)
+        step(s, stream0)
     torch.cuda.synchronize()
 
     # The timed steps run as one CUDA graph (no host launch overhead in the
-    # device timeline). The fused kernel is the only kernel in the graph, so
-    # its average launch duration is bounded by elapsed / launches (graph
-    # launch gaps included, i.e. a conservative figure).
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        stream = torch.cuda.current_stream()
-        for s in range(args.steps):
-            step(args.warmup + s)
-    stream = torch.cuda.current_stream()
-    graph.replay()  # warm replay (identical work)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        graph.replay()
-        t1.record(stream)
-        torch.cuda.synchronize()
-    elapsed_ms = t0.elapsed_time(t1)
-    if ws > 1:
-        tt = torch.tensor([elapsed_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt[0])
-        dist.barrier()
-    kern_ms = elapsed_ms / (args.steps * L)
+    # device timeline); kernel time per launch is bounded by elapsed / launches.
+    elapsed_ms, clocks = _timed_graph(torch, dist, ws, lambda s, st: step(args.warmup + s, st), args.steps, local,
+                                      sample_clocks=True)
+    launches_per_step = L * (3 if seqshard else 1)
     ms_per_step = elapsed_ms / args.steps
-    us_per_layer = ms_per_step * 1000.0 / L
-    del graph
+    tokens_per_layer = NS  # one decoded token per sequence per layer
+    us_per_token_layer = ms_per_step * 1000.0 / (L * tokens_per_layer)
+    kern_ms = elapsed_ms / (args.steps * L)  # per layer launch (all phases of the layer)
 
     # e2e through the public API with HOST buffers: per step the pinned H2D of
-    # q, k, v, the L decode launches and the D2H of the attention outputs, all
+    # q, k, v, the decode launches and the D2H of the attention outputs, all
     # captured as one graph (the way a serving loop drives the library).
-    hq = qs[:args.steps].cpu().pin_memory()
-    hk = ks[:args.steps].cpu().pin_memory()
-    hv = vs[:args.steps].cpu().pin_memory()
-    hout = torch.empty((args.steps, L, n_q, 128), dtype=torch.float32).pin_memory()
-    dq = torch.empty_like(qs[0])
-    dk = torch.empty_like(ks[0])
-    dv = torch.empty_like(vs[0])
+    n_e2e = min(args.steps, 16)
+    hq = qs[:n_e2e].cpu().pin_memory()
+    hk = ks[:n_e2e].cpu().pin_memory()
+    hv = vs[:n_e2e].cpu().pin_memory()
+    hout = torch.empty((n_e2e, L, NS, n_q, 128), dtype=torch.float32).pin_memory()
+    dq, dk, dv = torch.empty_like(qs[:1]), torch.empty_like(ks[:1]), torch.empty_like(vs[:1])
+    qs_save, ks_save, vs_save = qs, ks, vs
 
     def e2e_step(s, st):
-        dq.copy_(hq[s], non_blocking=True)
-        dk.copy_(hk[s], non_blocking=True)
-        dv.copy_(hv[s], non_blocking=True)
-        for l in range(L):
-            caches[l].decode_step(dq[l], dk[l], dv[l], B, out=out[l], want_idx=False, stream=st)
+        nonlocal qs, ks, vs
+        dq[0].copy_(hq[s], non_blocking=True)
+        dk[0].copy_(hk[s], non_blocking=True)
+        dv[0].copy_(hv[s], non_blocking=True)
+        qs, ks, vs = dq, dk, dv
+        step(0, st)
+        qs, ks, vs = qs_save, ks_save, vs_save
         hout[s].copy_(out, non_blocking=True)
-        for c in caches:
-            c.truncate(S - 1)
 
-    g2 = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g2):
-        st = torch.cuda.current_stream()
-        for s in range(args.steps):
-            e2e_step(s, st)
-    g2.replay()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    g2.replay()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if ws > 1:
-        tt = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt[0])
+    e2e_ms, _ = _timed_graph(torch, dist, ws, e2e_step, n_e2e, local)
     if not torch.isfinite(hout).all() and not int(os.environ.get("ADAMAS_DBG", "0")):
         raise SystemExit("non-finite attention output")
     h2d = (hq[0].numel() + hk[0].numel() + hv[0].numel()) * es
     d2h = hout[0].numel() * 4
 
     # roofline of the fused kernel: algorithmic bytes per launch
-    bytes_launch = n_kv * S * 32 + n_q * min(B, S) * 2 * 128 * es
+    bytes_launch = NS * (n_kv * S * 32 + n_q * min(B, S) * 2 * 128 * es)
+    if seqshard:  # this shard's survivors only: about B / 8 rows per q-head
+        bytes_launch = n_kv * S * 32 + n_q * (B // 8) * 2 * 128 * es
     achieved = bytes_launch / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = load_peaks()
-    traffic = load_traffic()
+    traffic = load_traffic() if args.config == "longchat" else None
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config == "longchat":
         try:
             v, threads, sample = cpu_reference(args, args.heads, args.cpu_steps, 2)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample}
@@ -319,22 +380,27 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     if rank == 0:
+        par = (f"sequence-shard x8 (rank {my_slot} of the split, world {ws})" if seqshard
+               else f"head-shard x{ws}")
         line = {
-            "metric": METRIC, "value": us_per_layer, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC, "value": us_per_token_layer, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"LongChat-7B attention decode: {args.heads} heads ({args.kv_heads} kv) x 128, "
-                                   f"S={S}, batch 1, budget {B}, {args.dtype} K/V, {L} layers per step",
-                       "layers_per_step": L, "heads_per_rank": n_q, "parallelism": f"head-shard x{ws}",
-                       "l2": "no flush: 32 distinct per-layer caches (17 GiB) > 126 MB L2"},
+            "config": {"workload": WORKLOAD[args.config].format(**vars(args)) + f", {args.dtype} K/V, "
+                                   f"{L} layers per step",
+                       "name": args.config, "layers_per_step": L, "sequences": NS, "heads_per_rank": n_q,
+                       "kv_heads_per_rank": n_kv, "parallelism": par,
+                       "us_per_layer_step": ms_per_step * 1000.0 / L,
+                       "l2": f"no flush: {L * NS} distinct per-(layer, request) caches, "
+                             f"{L * NS * n_kv * S * (256 * es + 32) / 2**30:.1f} GiB > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "fused_decode_kernel", "bytes_per_launch": bytes_launch,
                          "kernel_us": kern_ms * 1000.0, "peak_source": peak_kind},
-            "e2e": {"value": e2e_ms * 1000.0 / (args.steps * L), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "gpu_launches": args.steps * L,
-            "clocks": clk.summary(),
+            "e2e": {"value": e2e_ms * 1000.0 / (n_e2e * L * tokens_per_layer), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps * launches_per_step,
+            "clocks": clocks,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))

@@ -120,15 +120,18 @@ struct FusedSmem {
     stage = o; o += (uint32_t)stages * kStageBytes;
     dist = o;  o = align(o + (uint32_t)G * chunk * 2, 16);
     hist = o;  o += (uint32_t)G * kHistBins * 4;
-    hist_all = o; o += (uint32_t)C * G * kHistBins * 2;  // u16 histograms received from every rank
+    // u16 histograms received: from every rank for every head (one hop), or
+    // for the heads this rank owns only (two hops, C x G > 8)
+    const uint32_t owned_max = (uint32_t)((G + C - 1) / C);
+    hist_all = o; o += (C * G > 8 ? owned_max * C : (uint32_t)C * G) * kHistBins * 2;
     sel = o;   o = align(o + (uint32_t)G * selcap * 4, 16);
-    inbox = o; o += (uint32_t)C * G * kPartStride * 4;
+    inbox = o; o += owned_max * C * kPartStride * 4;  // partials of the heads this rank merges
     wpart = o; o += kConsumerWarps * kPartStride * 4;
     qf = o;    o += (uint32_t)G * kHeadDim * 4;  // the G query heads as fp32
     o = align(o, 32);
     qcode = o; o += (uint32_t)(G + 1) * 32;
     sq = o;    o += (uint32_t)(G + 1) * kHeadDim * 8;
-    bars = o;  o += (2 * kMaxStages + 2) * 8;  // full[], empty[], hist exchange, partial exchange
+    bars = o;  o += (2 * kMaxStages + 3) * 8;  // full[], empty[], hist / partial / threshold exchange
     total = o;
   }
 };
@@ -198,7 +201,9 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   constexpr int NT = kConsumers / G;      // consumer threads per q-head
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int scratch[2 * kConsumerWarps];
-  __shared__ int sc[kMaxG][4];  // per q-head: T, below, pre_lt, pre_eq
+  __shared__ __align__(16) int sc[kMaxG][4];  // per q-head: T, below, pre_lt, pre_eq
+  __shared__ int owner_sc[2];                  // two-hop exchange, owner side: T, below
+  __shared__ int rank_cnt[16][2];              // two-hop exchange, owner side: per rank (< T, == T)
   __shared__ int nsel[kMaxG];
   const int C = p.C;
   const int rank = (int)cluster_rank();
@@ -233,6 +238,8 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   uint64_t* empty_bar = full_bar + kMaxStages;
   uint64_t* hist_bar = full_bar + 2 * kMaxStages;
   uint64_t* inbox_bar = hist_bar + 1;
+  uint64_t* sc_bar = hist_bar + 2;
+  const bool two_hop = C * G > 8;  // histogram exchange topology (see the select phase)
   int n_owned = 0;  // q-heads whose final merge this rank performs
   for (int g = rank; g < G; g += C) ++n_owned;
 
@@ -269,11 +276,14 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     }
     mbar_init(hist_bar, 1);
     mbar_init(inbox_bar, 1);
+    mbar_init(sc_bar, 1);
     mbar_fence_init();
     for (int st = 0; st < min(ring, n_stages); ++st) issue(st);
     // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
     // C partials per q-head it merges
-    mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
+    if (!two_hop) mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
+    else if (n_owned) mbar_expect_tx(hist_bar, (uint32_t)(n_owned * C * kHistBins * 2));
+    if (two_hop) mbar_expect_tx(sc_bar, (uint32_t)(G * 16));
     if (n_owned && !p.cand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
   }
   // the G query heads (and the new key) are loaded before the barrier so the
@@ -388,29 +398,29 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   }
   consumer_sync();  // local histogram final
   ADAMAS_TRACE(3);
-  // Push this rank's histograms (as u16, counts <= chunk < 2^16) into every
-  // rank's hist_all[rank] with st.async; each receiver's mbarrier counts bytes.
-  cluster_wait();
-  if (tid < G * (kHistBins / 8)) {
-    const int g = tid / (kHistBins / 8), b0 = (tid % (kHistBins / 8)) * 8;
-    const int4 h0 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0);
-    const int4 h1 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0 + 4);
-    const uint32_t w0 = (uint32_t)h0.x | ((uint32_t)h0.y << 16), w1 = (uint32_t)h0.z | ((uint32_t)h0.w << 16);
-    const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)h1.w << 16);
-    const uint32_t local = smem_addr(hist_all + ((size_t)rank * G + g) * kHistBins + b0);
-    for (int r = 0; r < C; ++r)
-      st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), r));
-  }
-  mbar_wait(hist_bar, 0);
-  ADAMAS_TRACE(4);
-
-  // ---------------------------------------------------------------- threshold
-  // Head g's T = smallest distance whose cumulative count over all ranks
-  // reaches k. NT threads per head, G consecutive bins each; a head-segmented
-  // block prefix orders the threads; the owning thread walks its bins.
   const int k_eff = (int)min((int64_t)p.budget, S);
   const int g_me = tid / NT, t_in = tid % NT;
-  {
+  cluster_wait();
+  if (!two_hop) {
+    // One hop: every rank's histograms (u16: counts <= chunk < 2^16) go to
+    // every rank (st.async; each receiver's mbarrier counts bytes); each rank
+    // then derives, per head, T, the count below T and its own offsets.
+    if (tid < G * (kHistBins / 8)) {
+      const int g = tid / (kHistBins / 8), b0 = (tid % (kHistBins / 8)) * 8;
+      const int4 h0 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0);
+      const int4 h1 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0 + 4);
+      const uint32_t w0 = (uint32_t)h0.x | ((uint32_t)h0.y << 16), w1 = (uint32_t)h0.z | ((uint32_t)h0.w << 16);
+      const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)h1.w << 16);
+      const uint32_t local = smem_addr(hist_all + ((size_t)rank * G + g) * kHistBins + b0);
+      for (int r = 0; r < C; ++r)
+        st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), r));
+    }
+    mbar_wait(hist_bar, 0);
+    ADAMAS_TRACE(4);
+
+    // Head g's T = smallest distance whose cumulative count over all ranks
+    // reaches k. NT threads per head, G consecutive bins each; a head-segmented
+    // block prefix orders the threads; the owning thread walks its bins.
     const int b0 = t_in * G;
     int tot[G], pre[G];
 #pragma unroll
@@ -442,6 +452,50 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         cp += pre[i];
       }
     }
+  } else {
+    // Two hops (large C x G): head g's histograms go to its owner rank g % C
+    // only; the owner derives T and every rank's offsets and pushes each rank
+    // its (T, below, pre_lt, pre_eq).
+    if (tid < G * (kHistBins / 8)) {
+      const int g = tid / (kHistBins / 8), b0 = (tid % (kHistBins / 8)) * 8;
+      const int4 h0 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0);
+      const int4 h1 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0 + 4);
+      const uint32_t w0 = (uint32_t)h0.x | ((uint32_t)h0.y << 16), w1 = (uint32_t)h0.z | ((uint32_t)h0.w << 16);
+      const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)h1.w << 16);
+      const uint32_t owner = (uint32_t)(g % C), slot = (uint32_t)(g / C);
+      const uint32_t local = smem_addr(hist_all + ((size_t)slot * C + rank) * kHistBins + b0);
+      st_async_v4(mapa_shared(local, owner), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), owner));
+    }
+    if (n_owned) mbar_wait(hist_bar, 0);
+    ADAMAS_TRACE(4);
+    for (int j = 0; j < n_owned; ++j) {  // uniform within the CTA
+      const int g = rank + j * C;
+      const uint16_t* hs = hist_all + (size_t)j * C * kHistBins;
+      const int b = tid;  // one bin per consumer thread (kConsumers >= kHistBins)
+      int tot = 0;
+      if (b < kHistBins)
+        for (int r = 0; r < C; ++r) tot += hs[(size_t)r * kHistBins + b];
+      int c, unused0, tot_all, unused1;
+      head_scan2<1>(tot, 0, c, unused0, tot_all, unused1, scratch);
+      if (b < kHistBins && c < k_eff && c + tot >= k_eff) { owner_sc[0] = b; owner_sc[1] = c; }
+      consumer_sync();
+      const int T = owner_sc[0];
+      if (warp < C) {  // warp r: rank r's count below T and at T
+        int lt = 0;
+        for (int bb = lane; bb < T; bb += 32) lt += hs[(size_t)warp * kHistBins + bb];
+        lt = warp_sum_int(lt);
+        if (lane == 0) { rank_cnt[warp][0] = lt; rank_cnt[warp][1] = hs[(size_t)warp * kHistBins + T]; }
+      }
+      consumer_sync();
+      if (tid < C) {  // push (T, below, pre_lt, pre_eq) into rank tid's sc[g]
+        int pl = 0, pe = 0;
+        for (int r = 0; r < tid; ++r) { pl += rank_cnt[r][0]; pe += rank_cnt[r][1]; }
+        st_async_v4(mapa_shared(smem_addr(&sc[g][0]), (uint32_t)tid), (uint32_t)T, (uint32_t)owner_sc[1], (uint32_t)pl,
+                    (uint32_t)pe, mapa_shared(smem_addr(sc_bar), (uint32_t)tid));
+      }
+      consumer_sync();
+    }
+    mbar_wait(sc_bar, 0);
   }
   consumer_sync();
   ADAMAS_TRACE(5);
@@ -603,7 +657,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
       }
       // push (M, L, o[128]) into the merging rank's inbox[rank][g] (528 B)
-      const uint32_t local = smem_addr(inbox + (rank * G + g) * kPartStride);
+      const uint32_t local = smem_addr(inbox + ((g / C) * C + rank) * kPartStride);
       const uint32_t dst = mapa_shared(local, (uint32_t)(g % C));
       const uint32_t bar = mapa_shared(smem_addr(inbox_bar), (uint32_t)(g % C));
       if (lane == 0) st_async_v4(dst, __float_as_uint(M), __float_as_uint(Lsum), 0u, 0u, bar);
@@ -620,12 +674,12 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     if (g % C != rank) continue;
     float M = -INFINITY;
     for (int r = 0; r < C; ++r) {
-      const float* q2 = inbox + (r * G + g) * kPartStride;
+      const float* q2 = inbox + ((g / C) * C + r) * kPartStride;
       if (q2[1] > 0.f) M = fmaxf(M, q2[0]);
     }
     float Lsum = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int r = 0; r < C; ++r) {
-      const float* q2 = inbox + (r * G + g) * kPartStride;
+      const float* q2 = inbox + ((g / C) * C + r) * kPartStride;
       if (!(q2[1] > 0.f)) continue;
       const float c = exp2f(q2[0] - M);
       Lsum += q2[1] * c;

@@ -151,6 +151,8 @@ def run_decode(gpu, oracle, S, n_kv, G, budget, bf16, seed, steps=1):
     (5000, 1, 2, 9000, False),  # budget > S
     (4097, 1, 8, 128, True),
     (32768, 1, 1, 128, False),  # config 0: 1 head, 32K, fp32, budget 128
+    (32768, 2, 4, 128, True),   # Llama GQA group at 32K: C x G > 8, two-hop threshold exchange
+    (20000, 1, 8, 64, True),    # G = 8 (owners hold several heads when C < G)
 ])
 def test_fused_decode_step_matches_oracle(gpu, oracle, S, n_kv, G, budget, bf16):
     run_decode(gpu, oracle, S, n_kv, G, budget, bf16, seed=S + budget)
@@ -164,6 +166,14 @@ def test_fused_decode_multi_step(gpu, oracle):
 def test_fused_decode_cluster_sizes(gpu, oracle, monkeypatch, cluster):
     monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
     run_decode(gpu, oracle, 6000, 2, 1, 128, True, seed=int(cluster))
+
+
+@pytest.mark.parametrize("cluster,G", [("2", 4), ("4", 4), ("2", 8)])
+def test_fused_decode_exchange_topologies(gpu, oracle, monkeypatch, cluster, G):
+    """one-hop (C x G <= 8) and two-hop (C x G > 8) histogram exchanges,
+    including owners of several heads (G > C)"""
+    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    run_decode(gpu, oracle, 5000, 1, G, 96, True, seed=31 * G + int(cluster), steps=2)
 
 
 def test_operator_composition_matches_fused(gpu, oracle, monkeypatch):
