@@ -206,6 +206,83 @@ __device__ __forceinline__ bool encode128_warp(const float in[4], double* sq, Co
   return ok;
 }
 
+// fp32 route with a certified margin. The reference decides every code by
+// comparing fp64 values (y against -t, 0, +t, t = kQ28 sigma). Here y is the
+// same butterfly network in fp32 and sigma comes from the fp32 sum of x^2
+// (Parseval: sum y^2 = sum x^2 for the orthonormal transform). Rounding
+// bounds (7 stages of add + multiply, 128-term sums, u = 2^-24): every fp32 y
+// is within 14 u sqrt(128) sigma of the exact real value and the fp32
+// threshold within ~65 u sigma of the exact one; the reference's fp64 values
+// are within ~1e-14 sigma of the exact ones. A code is certain when y is
+// farther than E = 2^-15 sigma (~3.05e-5 sigma, > 2x the sum of those bounds)
+// from every threshold; otherwise (about 0.3 % of Gaussian vectors) — or for
+// scales where fp32 squares leave the normal range — the warp takes the exact
+// fp64 path above. Returns 1 certain / 0 degenerate (as encode128_warp) /
+// -1 not certified (out untouched).
+__device__ __forceinline__ int encode128_warp_f32(const float in[4], Code& out) {
+  const int lane = threadIdx.x & 31;
+  constexpr float c = 0.70710678118654752440f;
+  float x[4] = {in[0], in[1], in[2], in[3]};
+  float sq = __fmul_rn(x[0], x[0]);
+  sq = __fadd_rn(sq, __fmul_rn(x[1], x[1]));
+  sq = __fadd_rn(sq, __fmul_rn(x[2], x[2]));
+  sq = __fadd_rn(sq, __fmul_rn(x[3], x[3]));
+  {
+    const float a0 = x[0], b0 = x[1], a1 = x[2], b1 = x[3];
+    x[0] = __fmul_rn(__fadd_rn(a0, b0), c);
+    x[1] = __fmul_rn(__fsub_rn(a0, b0), c);
+    x[2] = __fmul_rn(__fadd_rn(a1, b1), c);
+    x[3] = __fmul_rn(__fsub_rn(a1, b1), c);
+  }
+  {
+    const float a0 = x[0], b0 = x[2], a1 = x[1], b1 = x[3];
+    x[0] = __fmul_rn(__fadd_rn(a0, b0), c);
+    x[2] = __fmul_rn(__fsub_rn(a0, b0), c);
+    x[1] = __fmul_rn(__fadd_rn(a1, b1), c);
+    x[3] = __fmul_rn(__fsub_rn(a1, b1), c);
+  }
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+    sq = __fadd_rn(sq, __shfl_xor_sync(kFull, sq, m));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float pj = __shfl_xor_sync(kFull, x[j], m);
+      x[j] = upper ? __fmul_rn(__fsub_rn(pj, x[j]), c) : __fmul_rn(__fadd_rn(x[j], pj), c);
+    }
+  }
+  // sq (warp-uniform) = sum x^2; usable range keeps every bound relative
+  if (!(sq > 1e-30f && sq < 1e37f)) return -1;
+  const float sigma = __fsqrt_rn(__fdiv_rn(sq, 128.f));
+  const float t = __fmul_rn(0.6744897501960817432f, sigma);
+  const float E = sigma * 3.0517578125e-5f;  // 2^-15 sigma
+  bool unsure = false;
+  uint32_t code[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float y = x[j], ay = fabsf(y);
+    unsure |= ay <= E || fabsf(ay - t) <= E;
+    code[j] = (uint32_t)(y > -t) + (uint32_t)(y > 0.f) + (uint32_t)(y > t);
+  }
+  if (__any_sync(kFull, unsure)) return -1;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    out.lo[j] = __ballot_sync(kFull, code[j] & 1u);
+    out.hi[j] = __ballot_sync(kFull, code[j] >> 1);
+  }
+  return 1;
+}
+
+// The encoder used on the hot paths: certified fp32, exact fp64 fallback.
+// exact = true forces the fp64 path (diagnostics / tests).
+__device__ __forceinline__ bool encode128(const float in[4], double* sq, Code& out, bool exact = false) {
+  if (!exact) {
+    const int r = encode128_warp_f32(in, out);
+    if (r >= 0) return r == 1;
+  }
+  return encode128_warp(in, sq, out, !exact);
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier + bulk-copy (TMA engine, non-tensor) helpers.
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     ADAMAS_TRACE(12);
     if (p.dbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
       for (int w = 0; w < 4; ++w) { c.lo[w] = __float_as_uint(f[w]); c.hi[w] = 0u; }
-    } else if (!encode128_warp(f, sqs + warp * kHeadDim, c, !p.exact_encode) && lane == 0) {
+    } else if (!encode128(f, sqs + warp * kHeadDim, c, p.exact_encode != 0) && lane == 0) {
       atomicOr(p.status, kStatusDegenerate);
     }
     if (lane == 0) qcode[warp] = c;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     float kf[4];
     Raw4<T>::to_float(kr, kf);
     Code c;
-    if (!encode128_warp(kf, sqs + G * kHeadDim, c, !p.exact_encode) && lane == 0)
+    if (!encode128(kf, sqs + G * kHeadDim, c, p.exact_encode != 0) && lane == 0)
       atomicOr(p.status, kStatusDegenerate);
     if (lane == 0) {
       qcode[G] = c;

@@ -97,7 +97,7 @@ append_kernel(const T* __restrict__ keys, const T* __restrict__ values,
     } else {
       float f[4];
       Raw4<T>::to_float(kr, f);
-      const bool ok = encode128_warp(f, sq[warp], c);
+      const bool ok = encode128(f, sq[warp], c);
       if (!ok && lane == 0) atomicOr(status, kStatusDegenerate);
     }
     if (lane == 0) store_code(codes + (int64_t)h * 2 * cap, cap, seq0 + t, c);
@@ -116,7 +116,7 @@ encode_query_kernel(const T* __restrict__ q, int n_q, uint16_t* __restrict__ out
   float f[4];
   Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)h * kHeadDim + lane * 4), f);
   Code c;
-  const bool ok = encode128_warp(f, sq[warp], c);
+  const bool ok = encode128(f, sq[warp], c);
   if (!ok && lane == 0) atomicOr(status, kStatusDegenerate);
   reinterpret_cast<uint8_t*>(out_ref + (int64_t)h * 16)[lane] = (uint8_t)ref_byte_from_planes(c, lane);
 }
