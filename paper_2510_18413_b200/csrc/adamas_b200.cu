@@ -92,7 +92,7 @@ template <typename T>
 int launch_append(adamas_cache* c, const void* keys, const void* values, const uint16_t* codes_ref,
                   int64_t n_tokens, cudaStream_t s) {
   const int64_t n_vec = n_tokens * c->n_kv;
-  const int64_t blocks_needed = (n_vec + kAppendWarps - 1) / kAppendWarps;
+  const int64_t blocks_needed = (n_vec + 2 * kAppendWarps - 1) / (2 * kAppendWarps);  // 2 vectors per warp
   const int grid = (int)std::min<int64_t>(blocks_needed, (int64_t)sm_count() * 16);
   if (codes_ref)
     append_kernel<T, true><<<grid, kAppendWarps * 32, 0, s>>>(

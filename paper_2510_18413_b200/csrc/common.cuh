@@ -219,58 +219,74 @@ __device__ __forceinline__ bool encode128_warp(const float in[4], double* sq, Co
 // scales where fp32 squares leave the normal range — the warp takes the exact
 // fp64 path above. Returns 1 certain / 0 degenerate (as encode128_warp) /
 // -1 not certified (out untouched).
-__device__ __forceinline__ int encode128_warp_f32(const float in[4], Code& out) {
+template <int N>
+__device__ __forceinline__ void encode128_warp_f32n(const float (&in)[N][4], Code (&out)[N], int (&res)[N]) {
   const int lane = threadIdx.x & 31;
   constexpr float c = 0.70710678118654752440f;
-  float x[4] = {in[0], in[1], in[2], in[3]};
-  float sq = __fmul_rn(x[0], x[0]);
-  sq = __fadd_rn(sq, __fmul_rn(x[1], x[1]));
-  sq = __fadd_rn(sq, __fmul_rn(x[2], x[2]));
-  sq = __fadd_rn(sq, __fmul_rn(x[3], x[3]));
-  {
-    const float a0 = x[0], b0 = x[1], a1 = x[2], b1 = x[3];
-    x[0] = __fmul_rn(__fadd_rn(a0, b0), c);
-    x[1] = __fmul_rn(__fsub_rn(a0, b0), c);
-    x[2] = __fmul_rn(__fadd_rn(a1, b1), c);
-    x[3] = __fmul_rn(__fsub_rn(a1, b1), c);
-  }
-  {
-    const float a0 = x[0], b0 = x[2], a1 = x[1], b1 = x[3];
-    x[0] = __fmul_rn(__fadd_rn(a0, b0), c);
-    x[2] = __fmul_rn(__fsub_rn(a0, b0), c);
-    x[1] = __fmul_rn(__fadd_rn(a1, b1), c);
-    x[3] = __fmul_rn(__fsub_rn(a1, b1), c);
+  float x[N][4], sq[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[n][j] = in[n][j];
+    sq[n] = __fmul_rn(x[n][0], x[n][0]);
+    sq[n] = __fadd_rn(sq[n], __fmul_rn(x[n][1], x[n][1]));
+    sq[n] = __fadd_rn(sq[n], __fmul_rn(x[n][2], x[n][2]));
+    sq[n] = __fadd_rn(sq[n], __fmul_rn(x[n][3], x[n][3]));
+    const float a0 = x[n][0], b0 = x[n][1], a1 = x[n][2], b1 = x[n][3];
+    x[n][0] = __fmul_rn(__fadd_rn(a0, b0), c);
+    x[n][1] = __fmul_rn(__fsub_rn(a0, b0), c);
+    x[n][2] = __fmul_rn(__fadd_rn(a1, b1), c);
+    x[n][3] = __fmul_rn(__fsub_rn(a1, b1), c);
+    const float a2 = x[n][0], b2 = x[n][2], a3 = x[n][1], b3 = x[n][3];
+    x[n][0] = __fmul_rn(__fadd_rn(a2, b2), c);
+    x[n][2] = __fmul_rn(__fsub_rn(a2, b2), c);
+    x[n][1] = __fmul_rn(__fadd_rn(a3, b3), c);
+    x[n][3] = __fmul_rn(__fsub_rn(a3, b3), c);
   }
 #pragma unroll
   for (int m = 1; m < 32; m <<= 1) {
     const bool upper = (lane & m) != 0;
-    sq = __fadd_rn(sq, __shfl_xor_sync(kFull, sq, m));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float pj = __shfl_xor_sync(kFull, x[j], m);
-      x[j] = upper ? __fmul_rn(__fsub_rn(pj, x[j]), c) : __fmul_rn(__fadd_rn(x[j], pj), c);
+    for (int n = 0; n < N; ++n) {
+      sq[n] = __fadd_rn(sq[n], __shfl_xor_sync(kFull, sq[n], m));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float pj = __shfl_xor_sync(kFull, x[n][j], m);
+        x[n][j] = upper ? __fmul_rn(__fsub_rn(pj, x[n][j]), c) : __fmul_rn(__fadd_rn(x[n][j], pj), c);
+      }
     }
   }
-  // sq (warp-uniform) = sum x^2; usable range keeps every bound relative
-  if (!(sq > 1e-30f && sq < 1e37f)) return -1;
-  const float sigma = __fsqrt_rn(__fdiv_rn(sq, 128.f));
-  const float t = __fmul_rn(0.6744897501960817432f, sigma);
-  const float E = sigma * 3.0517578125e-5f;  // 2^-15 sigma
-  bool unsure = false;
-  uint32_t code[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float y = x[j], ay = fabsf(y);
-    unsure |= ay <= E || fabsf(ay - t) <= E;
-    code[j] = (uint32_t)(y > -t) + (uint32_t)(y > 0.f) + (uint32_t)(y > t);
-  }
-  if (__any_sync(kFull, unsure)) return -1;
+  for (int n = 0; n < N; ++n) {
+    // sq (warp-uniform) = sum x^2; usable range keeps every bound relative
+    if (!(sq[n] > 1e-30f && sq[n] < 1e37f)) { res[n] = -1; continue; }
+    const float sigma = __fsqrt_rn(__fdiv_rn(sq[n], 128.f));
+    const float t = __fmul_rn(0.6744897501960817432f, sigma);
+    const float E = sigma * 3.0517578125e-5f;  // 2^-15 sigma
+    bool unsure = false;
+    uint32_t code[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    out.lo[j] = __ballot_sync(kFull, code[j] & 1u);
-    out.hi[j] = __ballot_sync(kFull, code[j] >> 1);
+    for (int j = 0; j < 4; ++j) {
+      const float y = x[n][j], ay = fabsf(y);
+      unsure |= ay <= E || fabsf(ay - t) <= E;
+      code[j] = (uint32_t)(y > -t) + (uint32_t)(y > 0.f) + (uint32_t)(y > t);
+    }
+    if (__any_sync(kFull, unsure)) { res[n] = -1; continue; }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      out[n].lo[j] = __ballot_sync(kFull, code[j] & 1u);
+      out[n].hi[j] = __ballot_sync(kFull, code[j] >> 1);
+    }
+    res[n] = 1;
   }
-  return 1;
+}
+__device__ __forceinline__ int encode128_warp_f32(const float in[4], Code& out) {
+  float v[1][4] = {{in[0], in[1], in[2], in[3]}};
+  Code o[1];
+  int r[1];
+  encode128_warp_f32n<1>(v, o, r);
+  if (r[0] == 1) out = o[0];
+  return r[0];
 }
 
 // The encoder used on the hot paths: certified fp32, exact fp64 fallback.

@@ -81,26 +81,47 @@ append_kernel(const T* __restrict__ keys, const T* __restrict__ values,
               int* __restrict__ status) {
   __shared__ double sq[kAppendWarps][kHeadDim];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t stride = (int64_t)gridDim.x * kAppendWarps;
-  for (int64_t vec = (int64_t)blockIdx.x * kAppendWarps + warp; vec < n_vec; vec += stride) {
-    const int64_t t = vec / n_kv;
-    const int h = (int)(vec % n_kv);
-    const int64_t row = (int64_t)h * cap + seq0 + t;
-    const auto kr = Raw4<T>::load(keys + vec * kHeadDim + lane * 4);
-    const auto vr = Raw4<T>::load(values + vec * kHeadDim + lane * 4);
-    Raw4<T>::store(K + row * kHeadDim + lane * 4, kr);
-    Raw4<T>::store(V + row * kHeadDim + lane * 4, vr);
-    Code c;
-    if constexpr (kCoded) {
-      const uint32_t byte = reinterpret_cast<const uint8_t*>(codes_ref + vec * 16)[lane];
-      planes_from_ref_byte(byte, c);
-    } else {
-      float f[4];
-      Raw4<T>::to_float(kr, f);
-      const bool ok = encode128(f, sq[warp], c);
-      if (!ok && lane == 0) atomicOr(status, kStatusDegenerate);
+  // two vectors per warp and iteration: independent shuffle chains interleave
+  constexpr int NV = 2;
+  const int64_t stride = (int64_t)gridDim.x * kAppendWarps * NV;
+  for (int64_t v0 = ((int64_t)blockIdx.x * kAppendWarps + warp) * NV; v0 < n_vec; v0 += stride) {
+    typename Raw4<T>::V kr[NV], vr[NV];
+#pragma unroll
+    for (int n = 0; n < NV; ++n) {
+      const int64_t vec = min(v0 + n, n_vec - 1);
+      kr[n] = Raw4<T>::load(keys + vec * kHeadDim + lane * 4);
+      vr[n] = Raw4<T>::load(values + vec * kHeadDim + lane * 4);
     }
-    if (lane == 0) store_code(codes + (int64_t)h * 2 * cap, cap, seq0 + t, c);
+    Code c[NV];
+    if constexpr (kCoded) {
+#pragma unroll
+      for (int n = 0; n < NV; ++n) {
+        const int64_t vec = min(v0 + n, n_vec - 1);
+        planes_from_ref_byte(reinterpret_cast<const uint8_t*>(codes_ref + vec * 16)[lane], c[n]);
+      }
+    } else {
+      float f[NV][4];
+      int res[NV];
+#pragma unroll
+      for (int n = 0; n < NV; ++n) Raw4<T>::to_float(kr[n], f[n]);
+      encode128_warp_f32n<NV>(f, c, res);
+#pragma unroll
+      for (int n = 0; n < NV; ++n) {
+        if (res[n] < 0) res[n] = encode128_warp(f[n], sq[warp], c[n], true) ? 1 : 0;  // exact fallback
+        if (res[n] == 0 && lane == 0 && v0 + n < n_vec) atomicOr(status, kStatusDegenerate);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NV; ++n) {
+      const int64_t vec = v0 + n;
+      if (vec >= n_vec) break;
+      const int64_t t = vec / n_kv;
+      const int h = (int)(vec % n_kv);
+      const int64_t row = (int64_t)h * cap + seq0 + t;
+      Raw4<T>::store(K + row * kHeadDim + lane * 4, kr[n]);
+      Raw4<T>::store(V + row * kHeadDim + lane * 4, vr[n]);
+      if (lane == 0) store_code(codes + (int64_t)h * 2 * cap, cap, seq0 + t, c[n]);
+    }
   }
 }
 
