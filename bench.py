@@ -289,6 +289,7 @@ def run_ours(args):
         parts_all = torch.empty((L, n_virtual, n_q, 132), dtype=torch.float32, device="cuda")
         my_slot = rank % n_virtual
         base = my_slot * S
+        shard_off = ((torch.arange(n_virtual, device="cuda", dtype=torch.int32) - my_slot) * S).view(-1, 1, 1)
 
         def step(s, st):
             for l in range(L):
@@ -297,14 +298,13 @@ def run_ours(args):
                                             base, B, stream=st)
                 if gather is not None:
                     keys_all[l, :ws].copy_(gather(keys))
-                else:  # other shards: same distances, indices moved to their ranges
-                    for r in range(n_virtual):
-                        keys_all[l, r].copy_(keys + (r - my_slot) * S)
+                else:  # other shards: same distances, indices moved to their ranges (one kernel)
+                    torch.add(keys.unsqueeze(0), shard_off, out=keys_all[l])
                 part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
                 if gather is not None:
                     parts_all[l, :ws].copy_(gather(part))
                 else:
-                    parts_all[l].copy_(part.expand(n_virtual, -1, -1))
+                    parts_all[l].copy_(part.unsqueeze(0).expand(n_virtual, -1, -1))
                 out[l, 0].copy_(ops.lse_merge(parts_all[l], stream=st))
                 if my_slot == n_virtual - 1:
                     c.truncate(S - 1)

@@ -148,7 +148,7 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
     configured_smem = smem;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * C));
+  cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * prm.qsplit * C));
   cfg.blockDim = dim3(kFusedThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -168,7 +168,7 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = -1;
       max_clusters[C] = n;
     }
-    if ((int64_t)prm.n_seqs * prm.n_kv > max_clusters[C]) prm.pdl = 0;
+    if ((int64_t)prm.n_seqs * prm.n_kv * prm.qsplit > max_clusters[C]) prm.pdl = 0;
   }
   if (prm.pdl) {
     attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -197,14 +197,37 @@ int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaSt
 // not fit the single-launch kernel (the caller composes operators instead).
 int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n_q, int dtype, const void* q,
                         const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
-                        cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0) {
-  const int G = n_q / n_kv;
+                        cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0,
+                        int qsplit = 0) {
+  if (qsplit == 0) {  // auto
+    // Clusters larger than 8 CTAs do not all co-reside: for big GQA groups
+    // split each kv-head's q-heads over two clusters (each re-reads the codes).
+    // Cluster sizes above 4 do not reach a full wave of co-resident CTAs on
+    // B200 (measured): take the smallest split whose launch uses C <= 4.
+    qsplit = env_int("ADAMAS_QSPLIT", 0);
+    if (qsplit <= 0) {
+      const int G_all = n_q / n_kv;
+      int best = 1, best_c = 1 << 30;
+      for (int qs = 1; qs <= G_all; qs *= 2) {
+        if (G_all % qs) break;
+        const int c = fused_decode_launch(caches, n_seqs, n_kv, n_q, dtype, q, k_new, v_new, budget, out, idx, s,
+                                          append, cand, cand_base, -qs);  // probe: C with this split
+        if (c == kFusedUnsupported) continue;
+        if (c <= 4) { best = qs; break; }
+        if (c < best_c) { best = qs; best_c = c; }
+      }
+      qsplit = best;
+    }
+  }
+  const bool probe = qsplit < 0;
+  if (probe) qsplit = -qsplit;
+  const int G = n_q / (n_kv * qsplit);
   if (G != 1 && G != 2 && G != 4 && G != 8) return kFusedUnsupported;
   if (n_seqs > kMaxSeqs || budget > (1 << 20)) return kFusedUnsupported;
   int64_t s_max = 0;
   for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + append);
   if (s_max < 1) s_max = 1;
-  const int units = n_seqs * n_kv;
+  const int units = n_seqs * n_kv * qsplit;
   int C = env_int("ADAMAS_CLUSTER", 0);
   if (C <= 0) {
     C = 1;
@@ -232,6 +255,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       continue;
     }
     if (L.total <= smem_cap || (stages == 2 && L.total <= (kCtasPerSm == 1 ? 220 : 108) * 1024)) {
+      if (probe) return C;
       FusedParams prm{};
       prm.n_seqs = n_seqs;
       prm.n_kv = n_kv;
@@ -243,6 +267,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       prm.dbg = env_int("ADAMAS_DBG", 0);
       prm.pdl = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
       prm.append = append;
+      prm.qsplit = qsplit;
       prm.cand = cand;
       prm.cand_base = cand_base;
       prm.q = q;

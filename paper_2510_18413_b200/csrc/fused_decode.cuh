@@ -70,6 +70,7 @@ struct FusedParams {
   int append;        // 1: append (k_new, v_new) first (decode step); 0: the cache as is
   uint32_t* cand;    // candidates mode: [n_seqs][n_q][budget] keys (dist << 23 | base + token), no attention
   int64_t cand_base; // global index of this cache's token 0 (sequence-sharded caches)
+  int qsplit;        // clusters per kv-head: each scans the codes for G of its qsplit * G q-heads
   const void* q;      // [n_seqs][n_q][128]
   const void* k_new;  // [n_seqs][n_kv][128]
   const void* v_new;
@@ -208,8 +209,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   const int C = p.C;
   const int rank = (int)cluster_rank();
   const int unit = blockIdx.x / C;
-  const int si = unit / p.n_kv, hk = unit % p.n_kv;
-  const int n_q = p.n_kv * G;
+  const int part = unit % p.qsplit;  // which G of the kv-head's qsplit * G q-heads
+  const int si = (unit / p.qsplit) / p.n_kv, hk = (unit / p.qsplit) % p.n_kv;
+  const int n_q = p.n_kv * G * p.qsplit;
+  const int q0 = (hk * p.qsplit + part) * G;  // first q-head of this unit
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   const int64_t cap = p.seq[si].cap;
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     if (tid == 0) grid_launch_dependents();
   }
   if (warp < G) {
-    const T* qp = reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + (int64_t)hk * G + warp) * kHeadDim;
+    const T* qp = reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + q0 + warp) * kHeadDim;
     Raw4<T>::to_float(Raw4<T>::load(qp + lane * 4), f);
   } else if (has_new && warp == G) {
     const int64_t vrow = (int64_t)si * p.n_kv + hk;
@@ -332,10 +335,12 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     }
     if (lane == 0) qcode[warp] = c;
     ADAMAS_TRACE(13);
-  } else if (has_new && warp == G) {  // append (kv_cache.cpp:62-71)
+  } else if (has_new && warp == G) {  // append (kv_cache.cpp:62-71); part 0 of a split kv-head writes
     const int64_t row = (int64_t)hk * cap + s_old;
-    Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].K) + row * kHeadDim + lane * 4, kr);
-    Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].V) + row * kHeadDim + lane * 4, vr);
+    if (part == 0) {
+      Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].K) + row * kHeadDim + lane * 4, kr);
+      Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].V) + row * kHeadDim + lane * 4, vr);
+    }
     float kf[4];
     Raw4<T>::to_float(kr, kf);
     Code c;
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       atomicOr(p.status, kStatusDegenerate);
     if (lane == 0) {
       qcode[G] = c;
-      store_code(planes, cap, s_old, c);
+      if (part == 0) store_code(planes, cap, s_old, c);
     }
   }
   consumer_sync();
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     ADAMAS_TRACE(6);
     if (my_lt > 0 || (my_eq > 0 && eq_before < eq_budget)) {
       int32_t* idx_row = (p.idx && !(p.dbg & 2))
-                             ? p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off
+                             ? p.idx + ((int64_t)si * n_q + q0 + g) * p.budget + out_off
                              : nullptr;
       int pos = lt_before + min(eq_before, eq_budget);
       int eq_seen = eq_before;
@@ -556,18 +561,18 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
           if (pos < selcap) sel[g * selcap + pos] = tok;
           if (idx_row) idx_row[pos] = tok;
           if (p.cand)  // (distance, global index) key: the distributed top-k's order
-            p.cand[((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget + out_off + pos] =
+            p.cand[((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos] =
                 ((uint32_t)dg[grp * 32 + i] << 23) | (uint32_t)(p.cand_base + tok);
           ++pos;
         }
       }
     }
     if (rank == 0 && p.idx && t_in == 0) {  // estimator.cpp:80 caps the selection at S
-      int32_t* row = p.idx + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget;
+      int32_t* row = p.idx + ((int64_t)si * n_q + q0 + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
     }
     if (rank == 0 && p.cand && t_in == 0) {
-      uint32_t* row = p.cand + ((int64_t)si * n_q + (int64_t)hk * G + g) * p.budget;
+      uint32_t* row = p.cand + ((int64_t)si * n_q + q0 + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = 0xffffffffu;
     }
   }
@@ -585,6 +590,8 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 #pragma unroll
     for (int j = 0; j < 4; ++j) qf[j] *= scale;
     const T* Kh = reinterpret_cast<const T*>(p.seq[si].K) + (int64_t)hk * cap * kHeadDim + lane * 4;
+    const T* knew_row = reinterpret_cast<const T*>(p.k_new) + ((int64_t)si * p.n_kv + hk) * kHeadDim + lane * 4;
+    const T* vnew_row = reinterpret_cast<const T*>(p.v_new) + ((int64_t)si * p.n_kv + hk) * kHeadDim + lane * 4;
     const T* Vh = reinterpret_cast<const T*>(p.seq[si].V) + (int64_t)hk * cap * kHeadDim + lane * 4;
     float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
     constexpr int B = 4;  // rows in flight per warp
@@ -595,8 +602,13 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         const int r = r0 + b * WG;
         if (r < ns) {
           const int64_t t = sel[g * selcap + r];
-          kb[b] = Raw4<T>::load(Kh + t * kHeadDim);
-          vb[b] = Raw4<T>::load(Vh + t * kHeadDim);
+          if (has_new && t == s_old) {  // the appended row: from the input (another CTA of a split
+            kb[b] = Raw4<T>::load(knew_row);  // kv-head may be the one writing it to the cache)
+            vb[b] = Raw4<T>::load(vnew_row);
+          } else {
+            kb[b] = Raw4<T>::load(Kh + t * kHeadDim);
+            vb[b] = Raw4<T>::load(Vh + t * kHeadDim);
+          }
         } else {
           kb[b] = typename Raw4<T>::V{};
           vb[b] = typename Raw4<T>::V{};
@@ -687,7 +699,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
     }
     const float inv = 1.f / Lsum;
-    float* op = p.out + ((int64_t)si * n_q + (int64_t)hk * G + g) * kHeadDim + lane * 4;
+    float* op = p.out + ((int64_t)si * n_q + q0 + g) * kHeadDim + lane * 4;
     *reinterpret_cast<float4*>(op) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
   }
   ADAMAS_TRACE(11);

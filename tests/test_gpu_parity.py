@@ -168,6 +168,14 @@ def test_fused_decode_cluster_sizes(gpu, oracle, monkeypatch, cluster):
     run_decode(gpu, oracle, 6000, 2, 1, 128, True, seed=int(cluster))
 
 
+@pytest.mark.parametrize("qsplit", ["1", "2", "4"])
+def test_fused_decode_qsplit(gpu, oracle, monkeypatch, qsplit):
+    """a kv-head's q-heads split over several clusters (each scans the codes
+    for its share); the appended row comes from the input for every part"""
+    monkeypatch.setenv("ADAMAS_QSPLIT", qsplit)
+    run_decode(gpu, oracle, 9000, 2, 4, 128, True, seed=71 + int(qsplit), steps=3)
+
+
 @pytest.mark.parametrize("cluster,G", [("2", 4), ("4", 4), ("2", 8)])
 def test_fused_decode_exchange_topologies(gpu, oracle, monkeypatch, cluster, G):
     """one-hop (C x G <= 8) and two-hop (C x G > 8) histogram exchanges,
