@@ -67,6 +67,63 @@ __global__ void __launch_bounds__(kFusedThreads, 1) probe(const uint16_t* src, i
       a = __popc(ml);
       b = __popc(me);
     }
+    if (MODE & 32) {  // per-thread SWAR "any <= T" over 16 tokens, rare detail branch
+      const int T = thr + (it & 1);
+      const uint32_t kle = ((uint32_t)T * 0x00010001u) | 0x80008000u;
+      const int t0 = tid * 16;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(dist + t0 + 8 * q);
+        const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((kle - w[e]) & 0x80008000u)) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int d = (int)((w[e] >> (16 * h)) & 0xffffu);
+            if (d > T) continue;
+            if (d < T) a += 1; else b += 1;
+          }
+        }
+      }
+    }
+    if (MODE & 64) {  // coalesced: thread reads 8-token words tid, tid + 512 (conflict-free LDS.128)
+      const int T = thr + (it & 1);
+      const uint32_t kle = ((uint32_t)T * 0x00010001u) | 0x80008000u;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int t0 = (q * kConsumers + tid) * 8;
+        const uint4 v4 = *reinterpret_cast<const uint4*>(dist + t0);
+        const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((kle - w[e]) & 0x80008000u)) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int d = (int)((w[e] >> (16 * h)) & 0xffffu);
+            if (d > T) continue;
+            if (d < T) a += 1; else b += 1;
+          }
+        }
+      }
+    }
+    if (MODE & 128) {  // as 64 but the any-test OR-reduced first (one branch per 8 tokens)
+      const int T = thr + (it & 1);
+      const uint32_t kle = ((uint32_t)T * 0x00010001u) | 0x80008000u;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int t0 = (q * kConsumers + tid) * 8;
+        const uint4 v4 = *reinterpret_cast<const uint4*>(dist + t0);
+        const uint32_t any = ((kle - v4.x) | (kle - v4.y) | (kle - v4.z) | (kle - v4.w)) & 0x80008000u;
+        if (any) {
+          const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+          for (int e = 0; e < 8; ++e) {
+            const int d = (int)((w[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+            if (d < T) a += 1; else if (d == T) b += 1;
+          }
+        }
+      }
+    }
     int x0 = a, x1 = b, x2 = 0, x3 = 0;
     if (MODE & 2) head_scan2<1>(a, b, x0, x1, x2, x3, scratch);
     if (MODE & 4) consumer_sync();
@@ -108,6 +165,9 @@ int main() {
   run<1 | 2 | 4>("group_masks + head_scan2 + sync", src, cyc, sink);
   run<8 | 4>("ballot masks + sync", src, cyc, sink);
   run<8 | 2 | 4>("ballot masks + head_scan2 + sync", src, cyc, sink);
+  run<32 | 4>("per-thread SWAR any-test (16 tok) + sync", src, cyc, sink);
+  run<64 | 4>("coalesced SWAR any-test + sync", src, cyc, sink);
+  run<128 | 4>("coalesced, OR-reduced any-test + sync", src, cyc, sink);
   run<16 | 4>("cooperative hot blocks + sync", src, cyc, sink);
   run<16 | 2 | 4>("cooperative hot blocks + head_scan2 + sync", src, cyc, sink);
   return 0;
