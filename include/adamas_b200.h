@@ -94,6 +94,19 @@ int adamas_cache_append_coded(adamas_cache* cache, const void* keys, const void*
 int adamas_cache_codes_ref(const adamas_cache* cache, int64_t start, int64_t n, uint16_t* out_ref,
                            void* stream);
 
+/* ADKV snapshot interchange (the reference's save_snapshot / load_snapshot,
+ * kv_cache.cpp:111-165; one file per kv-head, as the reference cache is one
+ * head): magic "ADKV", u32 version 1, u32 seq_len, u32 head_dim, u8 bits, f32
+ * keys, f32 values, u16 PackedCodes words. Save writes kv-head `kv_head`'s
+ * tokens [0, seq_len) (bf16 caches widen to f32 exactly); load appends the
+ * n_paths == n_kv_heads snapshots (equal lengths) with their code words
+ * verbatim (no re-encode; f32 values round to bf16 in a bf16 cache).
+ * I/O and format errors -> ADAMAS_ERR_RUNTIME (std::runtime_error in the
+ * reference); shapes this build does not hold (head_dim != 128, 1-bit) ->
+ * ADAMAS_ERR_CONFIG. Both synchronize `stream`. */
+int adamas_cache_save_adkv(const adamas_cache* cache, int kv_head, const char* path, void* stream);
+int adamas_cache_load_adkv(adamas_cache* cache, const char* const* paths, int n_paths, void* stream);
+
 /* ---------------------------------------------------------------- operators */
 
 /* pack(encode(q)) per q-head (sweep.cpp:92-94): q device [n_q_heads][128] in the

@@ -232,6 +232,47 @@ class Reference:
         L.ref_layer_build.restype = C.c_void_p
         L.ref_layer_free.argtypes = [C.c_void_p]
         L.ref_layer_decode.argtypes = [C.c_void_p, _SZ, C.c_int, C.c_int, C.POINTER(_D)]
+        L.ref_save_snapshot.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_load_snapshot.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
+        L.ref_load_snapshot.restype = C.c_void_p
+        L.ref_cache_rows.argtypes = [C.c_void_p, _SZ, C.POINTER(_D), C.POINTER(_D)]
+        L.ref_cache_code_words.argtypes = [C.c_void_p, _SZ, C.POINTER(C.c_uint16)]
+
+    # -- ADKV snapshots (kv_cache.cpp:111-165) ------------------------------------
+    def cache_from_rows(self, K, V, words):
+        """A reference KvCache (one head) holding rows K, V with the given code words."""
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        W = np.ascontiguousarray(words, dtype=np.uint16)
+        c = self.L.ref_cache_new(K.shape[1], 2)
+        for i in range(K.shape[0]):
+            if self.L.ref_cache_update(c, _p(K[i], _D), _p(V[i], _D), _p(W[i], C.c_uint16)):
+                raise ValueError("ConfigError: update")
+        return c
+
+    def save_snapshot(self, cache, path):
+        rc = self.L.ref_save_snapshot(cache, str(path).encode())
+        if rc:
+            raise (ValueError if rc == 1 else RuntimeError)("save_snapshot")
+
+    def load_snapshot(self, path):
+        """(K, V, words) of the reference's load_snapshot."""
+        rc = C.c_int(0)
+        c = self.L.ref_load_snapshot(str(path).encode(), C.byref(rc))
+        if rc.value:
+            raise (ValueError if rc.value == 1 else RuntimeError)("load_snapshot")
+        try:
+            n = self.L.ref_cache_seq_len(c)
+            K = np.zeros((n, 128)); V = np.zeros((n, 128)); W = np.zeros((n, 16), np.uint16)
+            for i in range(n):
+                self.L.ref_cache_rows(c, i, _p(K[i], _D), _p(V[i], _D))
+                self.L.ref_cache_code_words(c, i, _p(W[i], C.c_uint16))
+        finally:
+            self.L.ref_cache_free(c)
+        return K, V, W
+
+    def cache_free(self, cache):
+        self.L.ref_cache_free(cache)
 
     def simd_level(self) -> str:
         return self.L.ref_simd_level().decode()

@@ -149,6 +149,23 @@ int ref_cache_update(void* c, const double* k, const double* v, const uint16_t* 
 
 size_t ref_cache_seq_len(void* c) { return static_cast<KvCache*>(c)->seq_len(); }
 
+// save_snapshot / load_snapshot (kv_cache.cpp:111-165), for the ADKV interop tests.
+int ref_save_snapshot(void* c, const char* path) {
+  return guarded([&] { save_snapshot(*static_cast<KvCache*>(c), path); });
+}
+void* ref_load_snapshot(const char* path, int* rc) {
+  KvCache* out = nullptr;
+  *rc = guarded([&] { out = new KvCache(load_snapshot(path)); });
+  return out;
+}
+void ref_cache_rows(void* c, size_t i, double* key, double* value) {
+  auto* cache = static_cast<KvCache*>(c);
+  auto k = cache->key_row(i);
+  auto v = cache->value_row(i);
+  std::copy(k.begin(), k.end(), key);
+  std::copy(v.begin(), v.end(), value);
+}
+
 void ref_cache_code_words(void* c, size_t i, uint16_t* out) {
   auto w = static_cast<KvCache*>(c)->code_words(i);
   std::copy(w.begin(), w.end(), out);

@@ -87,6 +87,16 @@ class KvCache:
     def truncate(self, n: int) -> None:
         check(self.L.adamas_cache_truncate(self.h, n))
 
+    # -- ADKV snapshots (save_snapshot / load_snapshot, kv_cache.cpp:111-165) ----
+    def save_snapshot(self, kv_head: int, path: str, stream=None) -> None:
+        check(self.L.adamas_cache_save_adkv(self.h, kv_head, str(path).encode(), _stream(stream)))
+
+    def load_snapshots(self, paths, stream=None) -> int:
+        """Appends one reference snapshot per kv-head; returns seq_len."""
+        arr = (C.c_char_p * len(paths))(*[str(x).encode() for x in paths])
+        check(self.L.adamas_cache_load_adkv(self.h, arr, len(paths), _stream(stream)))
+        return self.seq_len
+
     def buffers(self):
         k, v, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(self.L.adamas_cache_buffers(self.h, C.byref(k), C.byref(v), C.byref(c)))

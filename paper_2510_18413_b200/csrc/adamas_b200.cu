@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <fstream>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -295,6 +296,29 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
 
 }  // namespace
 
+namespace {
+constexpr char kAdkvMagic[4] = {'A', 'D', 'K', 'V'};
+constexpr uint32_t kAdkvVersion = 1;
+
+float bf16_bits_to_float(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+uint16_t float_to_bf16_bits(float f) {  // round to nearest even (as the device conversion)
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x7fffffu)) return (uint16_t)((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+template <typename Tp>
+void put(std::ofstream& os, Tp v) { os.write(reinterpret_cast<const char*>(&v), sizeof(Tp)); }
+template <typename Tp>
+bool get(std::ifstream& is, Tp& v) { return (bool)is.read(reinterpret_cast<char*>(&v), sizeof(Tp)); }
+}  // namespace
+
 extern "C" {
 
 void adamas_debug_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
@@ -570,6 +594,124 @@ int adamas_lse_merge(const float* partials, int n_ranks, int n_q, float* out, vo
   if (!partials || !out) return fail(ADAMAS_ERR_CONFIG, "lse_merge: null pointer");
   lse_merge_kernel<<<n_q, 32, 0, as_stream(stream)>>>(partials, n_ranks, n_q, out);
   return launch_check("lse_merge_kernel");
+}
+
+// ---------------------------------------------------------------- ADKV snapshots
+// The reference's KvCache snapshot (kv_cache.cpp:111-165, README "KV
+// snapshots"): magic "ADKV", u32 version (1), u32 seq_len, u32 head_dim,
+// u8 bits, f32 keys [seq][d], f32 values [seq][d], u16 code words [seq][d/8].
+// One file per kv-head (the reference cache is one head).
+
+int adamas_cache_save_adkv(const adamas_cache* c, int kv_head, const char* path, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (kv_head < 0 || kv_head >= c->n_kv) return fail(ADAMAS_ERR_CONFIG, "save_adkv: kv_head out of range");
+  if (!path) return fail(ADAMAS_ERR_CONFIG, "save_adkv: null path");
+  const int64_t n = c->seq_len;
+  const size_t es = elem_size(c->dtype);
+  std::vector<uint8_t> kraw((size_t)n * kHeadDim * es), vraw(kraw.size());
+  std::vector<uint16_t> words((size_t)c->n_kv * n * 16);
+  uint16_t* dwords = nullptr;
+  cudaStream_t st = as_stream(stream);
+  if (n > 0) {
+    const char* kb = static_cast<const char*>(c->K) + (size_t)kv_head * c->capacity * kHeadDim * es;
+    const char* vb = static_cast<const char*>(c->V) + (size_t)kv_head * c->capacity * kHeadDim * es;
+    ADAMAS_CUDA(cudaMemcpyAsync(kraw.data(), kb, kraw.size(), cudaMemcpyDeviceToHost, st));
+    ADAMAS_CUDA(cudaMemcpyAsync(vraw.data(), vb, vraw.size(), cudaMemcpyDeviceToHost, st));
+    ADAMAS_CUDA(cudaMalloc(&dwords, words.size() * sizeof(uint16_t)));
+    int rc = adamas_cache_codes_ref(c, 0, n, dwords, stream);
+    if (rc == ADAMAS_OK) {
+      cudaError_t e = cudaMemcpyAsync(words.data(), dwords, words.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = fail(ADAMAS_ERR_RUNTIME, std::string("save_adkv: ") + cudaGetErrorString(e));
+    }
+    cudaFree(dwords);
+    if (rc != ADAMAS_OK) return rc;
+  }
+  std::ofstream os(path, std::ios::binary);
+  if (!os) return fail(ADAMAS_ERR_RUNTIME, std::string("save_adkv: cannot open ") + path);
+  os.write(kAdkvMagic, 4);
+  put(os, kAdkvVersion);
+  put(os, (uint32_t)n);
+  put(os, (uint32_t)kHeadDim);
+  put(os, (uint8_t)2);
+  for (const auto* raw : {&kraw, &vraw})
+    for (int64_t i = 0; i < n * kHeadDim; ++i) {
+      float f;
+      if (c->dtype == ADAMAS_BF16) f = bf16_bits_to_float(reinterpret_cast<const uint16_t*>(raw->data())[i]);
+      else f = reinterpret_cast<const float*>(raw->data())[i];
+      put(os, f);
+    }
+  const uint16_t* hw = words.data() + (size_t)kv_head * n * 16;
+  os.write(reinterpret_cast<const char*>(hw), (size_t)n * 16 * sizeof(uint16_t));
+  if (!os) return fail(ADAMAS_ERR_RUNTIME, std::string("save_adkv: write failed for ") + path);
+  return ADAMAS_OK;
+}
+
+int adamas_cache_load_adkv(adamas_cache* c, const char* const* paths, int n_paths, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (!paths || n_paths != c->n_kv) return fail(ADAMAS_ERR_CONFIG, "load_adkv: one snapshot per kv-head");
+  int64_t n = -1;
+  std::vector<std::vector<float>> K(n_paths), V(n_paths);
+  std::vector<std::vector<uint16_t>> W(n_paths);
+  for (int h = 0; h < n_paths; ++h) {
+    std::ifstream is(paths[h], std::ios::binary);
+    if (!is) return fail(ADAMAS_ERR_RUNTIME, std::string("load_adkv: cannot open ") + paths[h]);
+    char magic[4];
+    if (!is.read(magic, 4) || std::memcmp(magic, kAdkvMagic, 4) != 0)
+      return fail(ADAMAS_ERR_RUNTIME, "load_adkv: bad magic");
+    uint32_t version = 0, seq = 0, d = 0;
+    uint8_t bits = 0;
+    if (!get(is, version) || version != kAdkvVersion) return fail(ADAMAS_ERR_RUNTIME, "load_adkv: unknown version");
+    if (!get(is, seq) || !get(is, d) || !get(is, bits)) return fail(ADAMAS_ERR_RUNTIME, "load_adkv: truncated header");
+    if (bits != 1 && bits != 2) return fail(ADAMAS_ERR_RUNTIME, "load_adkv: unsupported code width");
+    if (d != kHeadDim || bits != 2)
+      return fail(ADAMAS_ERR_CONFIG, "load_adkv: adamas-b200 caches hold head_dim = 128, 2-bit codes");
+    if (n >= 0 && (int64_t)seq != n) return fail(ADAMAS_ERR_CONFIG, "load_adkv: snapshots differ in length");
+    n = seq;
+    K[h].resize((size_t)n * kHeadDim);
+    V[h].resize((size_t)n * kHeadDim);
+    W[h].resize((size_t)n * 16);
+    if (!is.read(reinterpret_cast<char*>(K[h].data()), K[h].size() * 4) ||
+        !is.read(reinterpret_cast<char*>(V[h].data()), V[h].size() * 4) ||
+        !is.read(reinterpret_cast<char*>(W[h].data()), W[h].size() * 2))
+      return fail(ADAMAS_ERR_RUNTIME, "load_adkv: truncated payload");
+  }
+  if (n <= 0) return ADAMAS_OK;
+  if (c->seq_len + n > c->capacity) return fail(ADAMAS_ERR_CONFIG, "load_adkv: cache capacity exceeded");
+  const size_t es = elem_size(c->dtype);
+  // token-major [n][n_kv][128] (the append layout); codes verbatim (no re-encode)
+  std::vector<uint8_t> hk((size_t)n * n_paths * kHeadDim * es), hv(hk.size());
+  std::vector<uint16_t> hw((size_t)n * n_paths * 16);
+  for (int64_t t = 0; t < n; ++t)
+    for (int h = 0; h < n_paths; ++h) {
+      const size_t dst = ((size_t)t * n_paths + h) * kHeadDim, src = (size_t)t * kHeadDim;
+      for (int e = 0; e < kHeadDim; ++e) {
+        if (c->dtype == ADAMAS_BF16) {
+          reinterpret_cast<uint16_t*>(hk.data())[dst + e] = float_to_bf16_bits(K[h][src + e]);
+          reinterpret_cast<uint16_t*>(hv.data())[dst + e] = float_to_bf16_bits(V[h][src + e]);
+        } else {
+          reinterpret_cast<float*>(hk.data())[dst + e] = K[h][src + e];
+          reinterpret_cast<float*>(hv.data())[dst + e] = V[h][src + e];
+        }
+      }
+      std::memcpy(&hw[((size_t)t * n_paths + h) * 16], &W[h][(size_t)t * 16], 32);
+    }
+  void *dk = nullptr, *dv = nullptr, *dw = nullptr;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMalloc(&dk, hk.size());
+  if (e == cudaSuccess) e = cudaMalloc(&dv, hv.size());
+  if (e == cudaSuccess) e = cudaMalloc(&dw, hw.size() * 2);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dk, hk.data(), hk.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dv, hv.data(), hv.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice, st);
+  int rc = e == cudaSuccess ? do_append(c, dk, dv, static_cast<const uint16_t*>(dw), n, stream)
+                            : fail(ADAMAS_ERR_RUNTIME, std::string("load_adkv: ") + cudaGetErrorString(e));
+  if (rc == ADAMAS_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    rc = fail(ADAMAS_ERR_RUNTIME, std::string("load_adkv: ") + cudaGetErrorString(e));
+  cudaFree(dk);
+  cudaFree(dv);
+  cudaFree(dw);
+  return rc;
 }
 
 void adamas_codes_ref_to_planes(const uint16_t* ref, int64_t n, uint32_t* planes) {

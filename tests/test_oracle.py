@@ -148,3 +148,19 @@ def test_bf16_round_matches_torch():
     import torch
     x = synth(17, 0, 4096) * 3.0
     assert np.array_equal(bf16_round(x), torch.from_numpy(x).to(torch.bfloat16).float().numpy())
+
+
+def test_reference_snapshot_round_trip(reference, oracle, tmp_path):
+    """The reference's own save_snapshot/load_snapshot through the shim (the
+    checker the ADKV interop tests rely on)."""
+    K = synth(91, 0, 40 * 128).reshape(40, 128)
+    V = synth(92, 0, 40 * 128).reshape(40, 128)
+    W = oracle.encode_pack_rows(K.astype(np.float64))
+    c = reference.cache_from_rows(K, V, W)
+    reference.save_snapshot(c, tmp_path / "r.adkv")
+    reference.cache_free(c)
+    Kr, Vr, Wr = reference.load_snapshot(tmp_path / "r.adkv")
+    assert np.array_equal(Kr, K.astype(np.float64)) and np.array_equal(Vr, V.astype(np.float64))
+    assert np.array_equal(Wr, W)
+    raw = (tmp_path / "r.adkv").read_bytes()
+    assert raw[:4] == b"ADKV" and len(raw) == 4 + 4 + 4 + 4 + 1 + 40 * 128 * 8 + 40 * 16 * 2
