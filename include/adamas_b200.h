@@ -119,6 +119,20 @@ int adamas_encode_query(const adamas_cache* cache, const void* q, int n_q_heads,
 int adamas_score(const adamas_cache* cache, const uint16_t* q_ref, int n_q_heads, int32_t* scores,
                  void* stream);
 
+/* Ablation metrics over the same cache (the reference's Metric, estimator.hpp:11,
+ * and its 1-bit pipeline, kernels.hpp:24-32):
+ *   ADAMAS_METRIC_MANHATTAN     = adamas_score
+ *   ADAMAS_METRIC_EUCLIDEAN_SQ  score_all(q, cache, Metric::euclidean_sq), 2-bit codes
+ *   ADAMAS_METRIC_HAMMING_1BIT  score_all over the 1-bit pipeline (pack(encode(x, 1)),
+ *                               l1_1bit): the 1-bit code is the 2-bit code's high bit
+ *                               (both threshold at 0), so the 2-bit cache serves it.
+ * q_ref: 2-bit reference words as for adamas_score. */
+#define ADAMAS_METRIC_MANHATTAN 0
+#define ADAMAS_METRIC_EUCLIDEAN_SQ 1
+#define ADAMAS_METRIC_HAMMING_1BIT 2
+int adamas_score_metric(const adamas_cache* cache, const uint16_t* q_ref, int n_q_heads, int metric,
+                        int32_t* scores, void* stream);
+
 /* top_k(scores, k) per row (estimator.cpp:75-90): the k smallest under the
  * order (score, index), ascending indices. scores device int32 [n_rows][n]
  * (values must lie in [0, 65535]); idx device int32 [n_rows][k]; entries past

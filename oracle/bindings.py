@@ -232,11 +232,39 @@ class Reference:
         L.ref_layer_build.restype = C.c_void_p
         L.ref_layer_free.argtypes = [C.c_void_p]
         L.ref_layer_decode.argtypes = [C.c_void_p, _SZ, C.c_int, C.c_int, C.POINTER(_D)]
+        L.ref_score_all_metric.argtypes = [C.c_void_p, C.POINTER(C.c_uint16), C.c_int, C.POINTER(C.c_int32)]
+        L.ref_encode_pack_bits.argtypes = [C.POINTER(_D), _SZ, C.c_int, C.POINTER(C.c_uint16)]
         L.ref_save_snapshot.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_load_snapshot.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
         L.ref_load_snapshot.restype = C.c_void_p
         L.ref_cache_rows.argtypes = [C.c_void_p, _SZ, C.POINTER(_D), C.POINTER(_D)]
         L.ref_cache_code_words.argtypes = [C.c_void_p, _SZ, C.POINTER(C.c_uint16)]
+
+    # -- ablation metrics (estimator.cpp:45-59, kernels.hpp:24-32) ---------------
+    def encode_pack_bits(self, x, bits):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.zeros(x.size * bits // 16, dtype=np.uint16)
+        if self.L.ref_encode_pack_bits(_p(x, _D), x.size, bits, _p(out, C.c_uint16)):
+            raise ValueError("ConfigError: encode")
+        return out
+
+    def score_all_metric(self, K, q, bits, metric):
+        """score_all(pack(encode(q, bits)), cache of K with bits-wide codes, metric)."""
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        c = self.L.ref_cache_new(K.shape[1], bits)
+        try:
+            zero = np.zeros(K.shape[1])
+            for i in range(K.shape[0]):
+                w = self.encode_pack_bits(K[i], bits)
+                if self.L.ref_cache_update(c, _p(K[i], _D), _p(zero, _D), _p(w, C.c_uint16)):
+                    raise ValueError("ConfigError: update")
+            qw = self.encode_pack_bits(q, bits)
+            out = np.zeros(K.shape[0], np.int32)
+            if self.L.ref_score_all_metric(c, _p(qw, C.c_uint16), metric, _p(out, C.c_int32)):
+                raise ValueError("ConfigError: score_all")
+            return out
+        finally:
+            self.L.ref_cache_free(c)
 
     # -- ADKV snapshots (kv_cache.cpp:111-165) ------------------------------------
     def cache_from_rows(self, K, V, words):

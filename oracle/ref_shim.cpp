@@ -183,6 +183,27 @@ int ref_score_all(void* c, const uint16_t* qwords, int32_t* out) {
   });
 }
 
+// score_all with any metric and the cache's own code width (1 or 2 bits).
+int ref_score_all_metric(void* c, const uint16_t* qwords, int metric, int32_t* out) {
+  auto* cache = static_cast<KvCache*>(c);
+  return guarded([&] {
+    PackedCodes q;
+    q.bits = cache->bits();
+    q.words.assign(qwords, qwords + cache->words_per_code());
+    q.len = q.words.size() * (16u / unsigned(q.bits));
+    auto s = score_all(q, *cache, metric ? Metric::euclidean_sq : Metric::manhattan);
+    std::copy(s.begin(), s.end(), out);
+  });
+}
+
+// pack(encode(x, bits)) (sweep.cpp:32-36) for bits 1 or 2.
+int ref_encode_pack_bits(const double* x, size_t d, int bits, uint16_t* words) {
+  return guarded([&] {
+    const auto p = pack(encode(std::span<const double>(x, d), bits));
+    std::copy(p.words.begin(), p.words.end(), words);
+  });
+}
+
 size_t ref_top_k(const int32_t* scores, size_t n, size_t k, int64_t* idx) {
   DistanceScores s(scores, scores + n);
   auto sel = top_k(s, k);

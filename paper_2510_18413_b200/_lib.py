@@ -25,6 +25,7 @@ EXPORTED = [
     "adamas_decode_step", "adamas_decode_step_batched", "adamas_codes_ref_to_planes",
     "adamas_codes_planes_to_ref", "adamas_debug_trace", "adamas_seq_local_candidates",
     "adamas_seq_select_attend", "adamas_lse_merge", "adamas_cache_save_adkv", "adamas_cache_load_adkv",
+    "adamas_score_metric",
 ]
 
 
@@ -72,6 +73,7 @@ def load() -> C.CDLL:
     L.adamas_seq_select_attend.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, vp, vp, vp]
     L.adamas_lse_merge.argtypes = [vp, i32, i32, vp, vp]
     L.adamas_cache_save_adkv.argtypes = [vp, i32, C.c_char_p, vp]
+    L.adamas_score_metric.argtypes = [vp, vp, i32, i32, vp, vp]
     L.adamas_cache_load_adkv.argtypes = [vp, C.POINTER(C.c_char_p), i32, vp]
     for name in EXPORTED:
         if not hasattr(L, name):

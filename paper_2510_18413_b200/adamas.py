@@ -156,11 +156,17 @@ class KvCache:
         check(self.L.adamas_encode_query(self.h, _ptr(q), n_q, _ptr(out), _stream(stream)))
         return out
 
-    def score_all(self, q_codes: torch.Tensor, stream=None) -> torch.Tensor:
-        """int32 [n_q][seq_len] Manhattan distances (estimator.cpp:45-59)."""
+    METRICS = {"manhattan": 0, "euclidean_sq": 1, "hamming_1bit": 2}
+
+    def score_all(self, q_codes: torch.Tensor, metric: str = "manhattan", stream=None) -> torch.Tensor:
+        """int32 [n_q][seq_len] distances (estimator.cpp:45-59): Metric::manhattan
+        (default), Metric::euclidean_sq, or the 1-bit pipeline's l1 ("hamming_1bit")."""
+        if metric not in self.METRICS:
+            raise ConfigError(f"unknown metric {metric}")
         n_q = q_codes.shape[0]
         out = torch.empty((n_q, self.seq_len), dtype=torch.int32, device="cuda")
-        check(self.L.adamas_score(self.h, _ptr(q_codes.contiguous()), n_q, _ptr(out), _stream(stream)))
+        check(self.L.adamas_score_metric(self.h, _ptr(q_codes.contiguous()), n_q, self.METRICS[metric], _ptr(out),
+                                         _stream(stream)))
         return out
 
     def sparse_attention(self, q: torch.Tensor, idx: torch.Tensor, with_lse: bool = False, stream=None):

@@ -449,8 +449,28 @@ int adamas_score(const adamas_cache* c, const uint16_t* q_ref, int n_q, int32_t*
   if (c->seq_len == 0) return ADAMAS_OK;  // estimator: empty cache -> empty scores
   const int64_t per_block = (int64_t)kScoreThreads * kScoreTokensPerThread;
   dim3 grid((unsigned)((c->seq_len + per_block - 1) / per_block), (unsigned)n_q);
-  score_kernel<<<grid, kScoreThreads, 0, as_stream(stream)>>>(c->codes, c->capacity, c->seq_len, n_q / c->n_kv,
-                                                             q_ref, scores);
+  score_kernel<kMetricManhattan><<<grid, kScoreThreads, 0, as_stream(stream)>>>(c->codes, c->capacity, c->seq_len,
+                                                                              n_q / c->n_kv, q_ref, scores);
+  return launch_check("score_kernel");
+}
+
+int adamas_score_metric(const adamas_cache* c, const uint16_t* q_ref, int n_q, int metric, int32_t* scores,
+                        void* stream) {
+  if (metric == ADAMAS_METRIC_MANHATTAN) return adamas_score(c, q_ref, n_q, scores, stream);
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (!q_ref || !scores) return fail(ADAMAS_ERR_CONFIG, "score_metric: null pointer");
+  if (metric != ADAMAS_METRIC_EUCLIDEAN_SQ && metric != ADAMAS_METRIC_HAMMING_1BIT)
+    return fail(ADAMAS_ERR_CONFIG, "score_metric: unknown metric");
+  if (c->seq_len == 0) return ADAMAS_OK;
+  const int64_t per_block = (int64_t)kScoreThreads * kScoreTokensPerThread;
+  dim3 grid((unsigned)((c->seq_len + per_block - 1) / per_block), (unsigned)n_q);
+  if (metric == ADAMAS_METRIC_EUCLIDEAN_SQ)
+    score_kernel<kMetricEuclideanSq><<<grid, kScoreThreads, 0, as_stream(stream)>>>(
+        c->codes, c->capacity, c->seq_len, n_q / c->n_kv, q_ref, scores);
+  else
+    score_kernel<kMetricHamming1><<<grid, kScoreThreads, 0, as_stream(stream)>>>(
+        c->codes, c->capacity, c->seq_len, n_q / c->n_kv, q_ref, scores);
   return launch_check("score_kernel");
 }
 

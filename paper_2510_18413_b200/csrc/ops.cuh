@@ -158,6 +158,36 @@ __global__ void codes_to_ref_kernel(const uint4* __restrict__ codes, int n_kv, i
 constexpr int kScoreThreads = 256;
 constexpr int kScoreTokensPerThread = 4;
 
+// Distance variants over the same bit planes (the
+// reference's ablations, kernels.hpp:24-32): with L = al ^ bl and
+// Hd = ah ^ bh = X ^ kx ^ L per element,
+//   manhattan (2-bit)      |a-b|   = L + 2 (Hd & ~(L & X))
+//   euclidean_sq (2-bit)   (a-b)^2 = L + 4 Hd + 4 (Hd & L & ~X) - 4 (Hd & L & X)
+//   1-bit L1 (Hamming)     [ah != bh] = Hd: the 1-bit code (x > 0) is the
+//                          2-bit code's high bit (both threshold at 0)
+constexpr int kMetricManhattan = 0;
+constexpr int kMetricEuclideanSq = 1;
+constexpr int kMetricHamming1 = 2;
+
+template <int METRIC>
+__device__ __forceinline__ uint32_t plane_distance(const QCode& q, const uint32_t klo[4], const uint32_t kx[4]) {
+  if (METRIC == kMetricManhattan) return l1_distance(q, klo, kx);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t L = q.lo[w] ^ klo[w];
+    const uint32_t Hd = q.x[w] ^ kx[w] ^ L;
+    if (METRIC == kMetricHamming1) {
+      acc += __popc(Hd);
+    } else {
+      const uint32_t cr = Hd & L;
+      acc += __popc(L) + 4u * __popc(Hd) + 4u * __popc(cr & ~q.x[w]) - 4u * __popc(cr & q.x[w]);
+    }
+  }
+  return acc;
+}
+
+template <int METRIC>
 __global__ void __launch_bounds__(kScoreThreads)
 score_kernel(const uint4* __restrict__ codes, int64_t cap, int64_t S, int group,
              const uint16_t* __restrict__ q_ref, int32_t* __restrict__ scores) {
@@ -182,7 +212,7 @@ score_kernel(const uint4* __restrict__ codes, int64_t cap, int64_t S, int group,
       uint32_t lo[4], x[4];
       ld_plane_nc(lo_plane + t, lo);
       ld_plane_nc(x_plane + t, x);
-      scores[(int64_t)hq * S + t] = (int32_t)l1_distance(q, lo, x);
+      scores[(int64_t)hq * S + t] = (int32_t)plane_distance<METRIC>(q, lo, x);
     }
   }
 }

@@ -252,3 +252,18 @@ def test_fast_encode_near_ties_and_scales(gpu, oracle):
         _, _, eidx, eout = oracle_decode(oracle, Kt, np.concatenate([V[:-1], V[-1:]]), q, budget)
         assert np.array_equal(idx.cpu().numpy(), eidx), trial
         cache.truncate(S - 1)
+
+
+@pytest.mark.parametrize("metric,bits,ref_metric", [("euclidean_sq", 2, 1), ("hamming_1bit", 1, 0)])
+def test_ablation_metrics_match_reference(gpu, reference, metric, bits, ref_metric):
+    """SURVEY 8f row f4: Metric::euclidean_sq over 2-bit codes and the 1-bit
+    pipeline's L1, from the same device cache, bit-exact against the
+    unmodified reference's score_all."""
+    S, n_kv, G = 1000, 1, 2
+    K, V, q = make_inputs(S, n_kv, n_kv * G, False, 23)
+    cache = fill_cache(gpu, K, V, False)
+    qw = cache.encode_query(to_dev(q, False))
+    got = cache.score_all(qw, metric=metric).cpu().numpy()
+    for h in range(n_kv * G):
+        exp = reference.score_all_metric(K[:, h // G], q[h], bits, ref_metric)
+        assert np.array_equal(got[h], exp), h

@@ -164,3 +164,28 @@ def test_reference_snapshot_round_trip(reference, oracle, tmp_path):
     assert np.array_equal(Wr, W)
     raw = (tmp_path / "r.adkv").read_bytes()
     assert raw[:4] == b"ADKV" and len(raw) == 4 + 4 + 4 + 4 + 1 + 40 * 128 * 8 + 40 * 16 * 2
+
+
+def test_plane_identities_for_ablation_metrics():
+    """(a-b)^2 = L + 4Hd + 4(Hd&L&~X) - 4(Hd&L&X) and [ah != bh] = Hd with
+    Hd = X ^ kx ^ L — the per-element identities behind adamas_score_metric."""
+    for a in range(4):
+        for b in range(4):
+            al, ah, bl, bh = a & 1, a >> 1, b & 1, b >> 1
+            L, X, kx = al ^ bl, al ^ ah, bl ^ bh
+            Hd = X ^ kx ^ L
+            assert Hd == ah ^ bh
+            cr = Hd & L
+            assert L + 4 * Hd + 4 * (cr & (1 - X)) - 4 * (cr & X) == (a - b) ** 2, (a, b)
+
+
+def test_one_bit_code_is_the_two_bit_high_bit(reference):
+    """The reference's 1-bit code (threshold {0}) equals the high bit of its
+    2-bit code, so 1-bit distances follow from the 2-bit cache."""
+    x = synth(77, 0, 64 * 128).reshape(64, 128).astype(np.float64)
+    for row in x:
+        w1 = reference.encode_pack_bits(row, 1)
+        w2 = reference.encode_pack_bits(row, 2)
+        c1 = np.array([(int(w1[i // 16]) >> (i % 16)) & 1 for i in range(128)])
+        c2 = np.array([(int(w2[i // 8]) >> (2 * (i % 8))) & 3 for i in range(128)])
+        assert np.array_equal(c1, c2 >> 1)
