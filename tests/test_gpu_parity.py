@@ -267,3 +267,46 @@ def test_ablation_metrics_match_reference(gpu, reference, metric, bits, ref_metr
     for h in range(n_kv * G):
         exp = reference.score_all_metric(K[:, h // G], q[h], bits, ref_metric)
         assert np.array_equal(got[h], exp), h
+
+
+def test_decode_errors_mirror_the_reference(gpu):
+    """ConfigError classes of the reference preconditions (common.hpp:19-22)."""
+    cache = gpu.KvCache(2, 3, torch.bfloat16)
+    kv = torch.randn((2, 128), device="cuda").bfloat16()
+    q3 = torch.randn((3, 128), device="cuda").bfloat16()
+    with pytest.raises(gpu.ConfigError):  # q-heads not a multiple of kv-heads
+        cache.decode_step(q3, kv, kv, 8)
+    q = torch.randn((4, 128), device="cuda").bfloat16()
+    with pytest.raises(gpu.ConfigError):  # empty selection (attention.cpp:42)
+        cache.decode_step(q, kv, kv, 0)
+    for _ in range(3):
+        cache.decode_step(q, kv, kv, 8)
+    with pytest.raises(gpu.ConfigError):  # capacity exhausted
+        cache.decode_step(q, kv, kv, 8)
+    with pytest.raises(gpu.ConfigError):  # dtype mismatch
+        gpu.KvCache(2, 8, torch.float32).decode_step(q, kv, kv, 8)
+
+
+def test_degenerate_query_latches_status_in_fused_step(gpu, oracle):
+    S = 300
+    K, V, _ = make_inputs(S, 1, 1, True, 61)
+    cache = fill_cache(gpu, K[:-1], V[:-1], True, capacity=S + 2)
+    assert cache.status() == 0
+    z = torch.zeros((1, 128), device="cuda").bfloat16()
+    cache.decode_step(z, to_dev(K[-1], True), to_dev(V[-1], True), 16)
+    with pytest.raises(gpu.ConfigError):  # quantizer.cpp:46-47: zero vector
+        cache.raise_on_degenerate()
+
+
+def test_seq_shard_empty_rank_and_errors(gpu, oracle):
+    from paper_2510_18413_b200.seqshard import CudaSeqOps
+    ops = CudaSeqOps()
+    c = gpu.KvCache(1, 8, torch.bfloat16)
+    q = torch.randn((2, 128), device="cuda").bfloat16()
+    keys = ops.local_candidates(c, q, None, None, False, 0, 16)  # empty shard: no candidates
+    assert (keys.cpu().numpy().view(np.uint32) == 0xFFFFFFFF).all()
+    g = torch.stack([keys, keys])
+    with pytest.raises(gpu.ConfigError):  # n_ranks * budget > 8192
+        ops.select_attend(c, q, torch.stack([keys] * 2).repeat(1, 1, 300)[:, :, :4800], 4800, 10, 0)
+    part, gidx = ops.select_attend(c, q, g, 16, 1, 0, want_idx=True)  # nothing selected here
+    assert (gidx.cpu().numpy() == -1).all() and (part[:, 1].cpu().numpy() == 0).all()
