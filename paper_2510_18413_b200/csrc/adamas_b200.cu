@@ -28,6 +28,12 @@ struct adamas_cache {
   void* V = nullptr;
   uint4* codes = nullptr;  // [n_kv][2 planes][capacity] x 16 B
   int* status = nullptr;  // device sticky status word
+  // multi-cluster units: [unit][4] barrier words (zeroed once), lazily sized
+  // histogram / partial scratch
+  int* xsync = nullptr;
+  uint32_t* xhist = nullptr;
+  float* xpart = nullptr;
+  size_t x_unit_heads = 0;  // (unit, cluster, head) slots the scratch holds
   // decode scratch (lazily grown)
   int32_t* scores = nullptr;
   size_t scores_elems = 0;
@@ -136,6 +142,21 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+// Global scratch of multi-cluster units (not during graph capture: the first
+// eager launch of a shape sizes it).
+int ensure_unit_scratch(adamas_cache* c, size_t slots) {
+  if (c->x_unit_heads >= slots) return ADAMAS_OK;
+  cudaFree(c->xhist);
+  cudaFree(c->xpart);
+  c->xhist = nullptr;
+  c->xpart = nullptr;
+  c->x_unit_heads = 0;
+  ADAMAS_CUDA(cudaMalloc(&c->xhist, slots * kHistBins * sizeof(uint32_t)));
+  ADAMAS_CUDA(cudaMalloc(&c->xpart, slots * kPartStride * sizeof(float)));
+  c->x_unit_heads = slots;
+  return ADAMAS_OK;
+}
+
 // ----------------------------------------------------------------- fused launcher
 template <typename T, int G>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
@@ -149,7 +170,7 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
     configured_smem = smem;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * prm.qsplit * C));
+  cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * prm.qsplit * prm.P * C));
   cfg.blockDim = dim3(kFusedThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -169,7 +190,15 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = -1;
       max_clusters[C] = n;
     }
-    if ((int64_t)prm.n_seqs * prm.n_kv * prm.qsplit > max_clusters[C]) prm.pdl = 0;
+    if ((int64_t)prm.n_seqs * prm.n_kv * prm.qsplit * prm.P > max_clusters[C]) prm.pdl = 0;
+  }
+  if (prm.P > 1) {  // spin barriers between the clusters of a unit: every cluster must be resident at once
+    if (max_clusters[C] == 0) {
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = -1;
+      max_clusters[C] = n;
+    }
+    if ((int64_t)prm.n_seqs * prm.n_kv * prm.qsplit * prm.P > max_clusters[C]) return kFusedUnsupported;
   }
   if (prm.pdl) {
     attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -201,10 +230,9 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
                         cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0,
                         int qsplit = 0) {
   if (qsplit == 0) {  // auto
-    // Clusters larger than 8 CTAs do not all co-reside: for big GQA groups
-    // split each kv-head's q-heads over two clusters (each re-reads the codes).
-    // Cluster sizes above 4 do not reach a full wave of co-resident CTAs on
-    // B200 (measured): take the smallest split whose launch uses C <= 4.
+    // Clusters above 4 CTAs do not reach a full wave of co-resident CTAs on
+    // B200 (measured): take the smallest split of a kv-head's q-heads over
+    // clusters (each re-reads the codes) whose launch uses C <= 4.
     qsplit = env_int("ADAMAS_QSPLIT", 0);
     if (qsplit <= 0) {
       const int G_all = n_q / n_kv;
@@ -229,30 +257,39 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
   for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + append);
   if (s_max < 1) s_max = 1;
   const int units = n_seqs * n_kv * qsplit;
+  // C CTAs per cluster, P clusters per unit. P > 1 (opt-in, ADAMAS_P)
+  // exchanges histograms and partials through global memory with a
+  // self-resetting barrier; it is exact but measured slower than splitting
+  // the q-heads (qsplit), so the automatic choice grows C only.
   int C = env_int("ADAMAS_CLUSTER", 0);
   if (C <= 0) {
     C = 1;
     while (C < 16 && units * C * 2 <= sm_count()) C *= 2;
   }
+  int P = std::max(1, env_int("ADAMAS_P", 1));
+  auto grow = [&]() {  // more CTAs per unit; false when out of options
+    if (C < 16) { C *= 2; return true; }
+    return false;
+  };
   for (;;) {
-    int64_t chunk = (s_max + C - 1) / C;
+    int64_t chunk = (s_max + (int64_t)C * P - 1) / ((int64_t)C * P);
     chunk = (chunk + 255) / 256 * 256;
     const int selcap = (int)std::min<int64_t>(budget, chunk);
     // one CTA per SM when the grid fits the machine, else two (always two
     // with the 8-warp build, so consecutive launches co-reside)
-    size_t smem_cap = kCtasPerSm == 1 && (size_t)units * C <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
+    size_t smem_cap =
+        kCtasPerSm == 1 && (size_t)units * C * P <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
     if (env_int("ADAMAS_SMEM_KB", 0) > 0) smem_cap = (size_t)env_int("ADAMAS_SMEM_KB", 0) * 1024;  // experiments
-    const FusedSmem base(G, C, (int)chunk, selcap, 0);
+    const FusedSmem base(G, C, (int)chunk, selcap, 0, P);
     const int want = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (chunk + kStageTok - 1) / kStageTok));
     int stages = env_int("ADAMAS_STAGES", 0);
     if (stages <= 0) {
       stages = want;
       while (stages > 2 && base.total + (size_t)stages * kStageTok * 32 > smem_cap) --stages;
     }
-    const FusedSmem L(G, C, (int)chunk, selcap, stages);
+    const FusedSmem L(G, C, (int)chunk, selcap, stages, P);
     if (chunk > 65280) {  // u16 histogram exchange: per-rank counts must stay < 2^16
-      if (C >= 16) return kFusedUnsupported;
-      C *= 2;
+      if (!grow()) return kFusedUnsupported;
       continue;
     }
     if (L.total <= smem_cap || (stages == 2 && L.total <= (kCtasPerSm == 1 ? 220 : 108) * 1024)) {
@@ -269,6 +306,10 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
       prm.pdl = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
       prm.append = append;
       prm.qsplit = qsplit;
+      prm.P = P;
+      if (P > 1)
+        for (int i = 0; i < n_seqs; ++i)
+          if (int rc = ensure_unit_scratch(caches[i], (size_t)n_kv * qsplit * P * G)) return rc;
       prm.cand = cand;
       prm.cand_base = cand_base;
       prm.q = q;
@@ -285,12 +326,14 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
         prm.seq[i].cap = caches[i]->capacity;
         prm.seq[i].s_old = caches[i]->seq_len;
         prm.seq[i].clean = std::min(caches[i]->dirty_from, caches[i]->seq_len);
+        prm.seq[i].xhist = caches[i]->xhist;
+        prm.seq[i].xpart = caches[i]->xpart;
+        prm.seq[i].xsync = caches[i]->xsync;
       }
       return dtype == ADAMAS_BF16 ? launch_fused_dtype<__nv_bfloat16>(prm, G, C, L.total, s)
                                   : launch_fused_dtype<float>(prm, G, C, L.total, s);
     }
-    if (C >= 16) return kFusedUnsupported;
-    C *= 2;
+    if (!grow()) return kFusedUnsupported;
   }
 }
 
@@ -354,6 +397,8 @@ int adamas_cache_create(adamas_cache** out, int n_kv_heads, int head_dim, int bi
   if (e == cudaSuccess) e = cudaMalloc(&c->codes, rows * 2 * sizeof(uint4));
   if (e == cudaSuccess) e = cudaMalloc(&c->status, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->status, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->xsync, (size_t)n_kv_heads * kMaxG * 4 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->xsync, 0, (size_t)n_kv_heads * kMaxG * 4 * sizeof(int));
   if (e != cudaSuccess) {
     adamas_cache_destroy(c);
     return fail(ADAMAS_ERR_RUNTIME, std::string("cache allocation: ") + cudaGetErrorString(e));
@@ -368,6 +413,9 @@ int adamas_cache_destroy(adamas_cache* c) {
   cudaFree(c->V);
   cudaFree(c->codes);
   cudaFree(c->status);
+  cudaFree(c->xsync);
+  cudaFree(c->xhist);
+  cudaFree(c->xpart);
   cudaFree(c->scores);
   cudaFree(c->qref);
   cudaFree(c->idx);
@@ -524,6 +572,8 @@ int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const vo
                ? kFusedUnsupported
                : fused_decode_launch(caches, n_seqs, c0->n_kv, n_q, c0->dtype, q, k_new, v_new, budget, out, idx,
                                      as_stream(stream));
+  if (rc == kFusedUnsupported && env_int("ADAMAS_REQUIRE_FUSED", 0))
+    return fail(ADAMAS_ERR_CONFIG, "decode: shape not supported by the fused kernel (ADAMAS_REQUIRE_FUSED)");
   if (rc == kFusedUnsupported) {
     // Operator composition (same semantics, several launches).
     for (int i = 0; i < n_seqs; ++i) {

@@ -28,6 +28,7 @@ constexpr double kQ28 = 0.6744897501960817432;
 
 // Sticky status bits (C-ABI ADAMAS_STATUS_*).
 constexpr int kStatusDegenerate = 1;  // zero or non-finite vector (quantizer.cpp:46-47)
+constexpr int kStatusSyncTimeout = 4;  // a multi-cluster unit barrier gave up (results invalid)
 
 struct __align__(32) Code {
   uint32_t lo[4];

@@ -60,6 +60,10 @@ struct FusedSeq {
   int64_t cap;
   int64_t s_old;  // tokens in the cache before this step's append
   int64_t clean;  // tokens [0, clean) were not written by the preceding kernel: streamable before the PDL wait
+  // multi-cluster units (FusedParams::P > 1): global scratch of this cache
+  uint32_t* xhist;  // [unit][P][G][kHistBins] cluster-combined histograms
+  float* xpart;     // [unit][P][G][kPartStride] cluster partials
+  int* xsync;       // [unit][4]: histogram barrier (count, generation), partial barrier (count, generation)
 };
 
 struct FusedParams {
@@ -71,6 +75,7 @@ struct FusedParams {
   uint32_t* cand;    // candidates mode: [n_seqs][n_q][budget] keys (dist << 23 | base + token), no attention
   int64_t cand_base; // global index of this cache's token 0 (sequence-sharded caches)
   int qsplit;        // clusters per kv-head: each scans the codes for G of its qsplit * G q-heads
+  int P;             // clusters per unit (token ranges); > 1 exchanges through global memory
   const void* q;      // [n_seqs][n_q][128]
   const void* k_new;  // [n_seqs][n_kv][128]
   const void* v_new;
@@ -109,6 +114,33 @@ __device__ __forceinline__ unsigned long long trace_clock(int dbg) {
     }                                                                                   \
   } while (0)
 
+// Self-resetting barrier among the CTAs of one multi-cluster unit (one
+// thread per CTA; all of them co-resident: the launcher keeps such grids to
+// one wave). The generation is read before arriving; the last arriver resets
+// the count and advances the generation. Writes before the arrival are made
+// visible (fence); waiters give up after ~1 s and latch a status bit rather
+// than hang.
+__device__ __forceinline__ void unit_barrier(int* bar, int target, bool wait, int* status) {
+  volatile int* gen = bar + 1;
+  const int g0 = *gen;
+  __threadfence();
+  const int old = atomicAdd(bar, 1);
+  if (old == target - 1) {
+    atomicExch(bar, 0);
+    __threadfence();
+    atomicAdd(bar + 1, 1);
+  } else if (wait) {
+    for (long long spin = 0; *gen == g0; ++spin) {
+      if (spin > (1LL << 24)) {
+        atomicOr(status, kStatusSyncTimeout);
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  __threadfence();
+}
+
 // Named barrier over the 16 consumer warps (the producer warp never joins).
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
@@ -116,7 +148,7 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;"
 struct FusedSmem {
   uint32_t stage, dist, hist, hist_all, sel, inbox, wpart, qf, qcode, sq, bars, total;
   __host__ __device__ static uint32_t align(uint32_t x, uint32_t a) { return (x + a - 1u) & ~(a - 1u); }
-  __host__ __device__ FusedSmem(int G, int C, int chunk, int selcap, int stages) {
+  __host__ __device__ FusedSmem(int G, int C, int chunk, int selcap, int stages, int P = 1) {
     uint32_t o = 0;
     stage = o; o += (uint32_t)stages * kStageBytes;
     dist = o;  o = align(o + (uint32_t)G * chunk * 2, 16);
@@ -124,7 +156,7 @@ struct FusedSmem {
     // u16 histograms received: from every rank for every head (one hop), or
     // for the heads this rank owns only (two hops, C x G > 8)
     const uint32_t owned_max = (uint32_t)((G + C - 1) / C);
-    hist_all = o; o += (C * G > 8 ? owned_max * C : (uint32_t)C * G) * kHistBins * 2;
+    hist_all = o; o += (C * G > 8 || P > 1 ? owned_max * C : (uint32_t)C * G) * kHistBins * 2;
     sel = o;   o = align(o + (uint32_t)G * selcap * 4, 16);
     inbox = o; o += owned_max * C * kPartStride * 4;  // partials of the heads this rank merges
     wpart = o; o += kConsumerWarps * kPartStride * 4;
@@ -205,10 +237,14 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   __shared__ __align__(16) int sc[kMaxG][4];  // per q-head: T, below, pre_lt, pre_eq
   __shared__ int owner_sc[2];                  // two-hop exchange, owner side: T, below
   __shared__ int rank_cnt[16][2];              // two-hop exchange, owner side: per rank (< T, == T)
+  __shared__ int cl_cnt[2];                    // multi-cluster unit: earlier clusters' (< T, == T)
   __shared__ int nsel[kMaxG];
   const int C = p.C;
   const int rank = (int)cluster_rank();
-  const int unit = blockIdx.x / C;
+  const int P = p.P;
+  const int pc = (blockIdx.x / C) % P;  // this cluster's token range within the unit
+  const int gr = pc * C + rank;          // rank over the unit's P * C CTAs
+  const int unit = blockIdx.x / (C * P);
   const int part = unit % p.qsplit;  // which G of the kv-head's qsplit * G q-heads
   const int si = (unit / p.qsplit) / p.n_kv, hk = (unit / p.qsplit) % p.n_kv;
   const int n_q = p.n_kv * G * p.qsplit;
@@ -218,7 +254,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   const int64_t cap = p.seq[si].cap;
   const int64_t s_old = p.seq[si].s_old;
   const int64_t S = s_old + (p.append ? 1 : 0);
-  const int64_t start = (int64_t)rank * p.chunk;
+  const int64_t start = (int64_t)gr * p.chunk;
   const int64_t end = min(S, start + (int64_t)p.chunk);
   const int len = end > start ? (int)(end - start) : 0;
   const int mem_len = (int)max((int64_t)0, min(end, s_old) - start);  // already in HBM
@@ -226,7 +262,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   const int selcap = min(p.budget, p.chunk);
   const int ring = p.stages;
 
-  const FusedSmem L(G, C, p.chunk, selcap, ring);
+  const FusedSmem L(G, C, p.chunk, selcap, ring, p.P);
   uint4* stage = reinterpret_cast<uint4*>(smem + L.stage);
   uint16_t* dist = reinterpret_cast<uint16_t*>(smem + L.dist);
   int* hist = reinterpret_cast<int*>(smem + L.hist);
@@ -242,7 +278,9 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   uint64_t* hist_bar = full_bar + 2 * kMaxStages;
   uint64_t* inbox_bar = hist_bar + 1;
   uint64_t* sc_bar = hist_bar + 2;
-  const bool two_hop = C * G > 8;  // histogram exchange topology (see the select phase)
+  const bool two_hop = C * G > 8 || P > 1;  // histogram exchange topology (see the select phase)
+  const int xunit = hk * p.qsplit + part;     // this cache's unit index (global scratch)
+  const int owners = min(C, G);               // ranks of a cluster that own a head
   int n_owned = 0;  // q-heads whose final merge this rank performs
   for (int g = rank; g < G; g += C) ++n_owned;
 
@@ -473,16 +511,48 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     }
     if (n_owned) mbar_wait(hist_bar, 0);
     ADAMAS_TRACE(4);
+    if (P > 1 && n_owned) {
+      // Multi-cluster unit: publish this cluster's combined histogram of each
+      // owned head, then one arrival per owner CTA on the unit's barrier.
+      for (int j = 0; j < n_owned; ++j) {
+        const int g = rank + j * C;
+        const uint16_t* hs = hist_all + (size_t)j * C * kHistBins;
+        uint32_t* dst = p.seq[si].xhist + (((size_t)xunit * P + pc) * G + g) * kHistBins;
+        for (int b = tid; b < kHistBins; b += kConsumers) {
+          uint32_t t = 0;
+          for (int r = 0; r < C; ++r) t += hs[(size_t)r * kHistBins + b];
+          __stcg(dst + b, t);
+        }
+      }
+      consumer_sync();
+      if (tid == 0) unit_barrier(p.seq[si].xsync + xunit * 4, P * owners, true, p.status);
+      consumer_sync();
+    }
     for (int j = 0; j < n_owned; ++j) {  // uniform within the CTA
       const int g = rank + j * C;
       const uint16_t* hs = hist_all + (size_t)j * C * kHistBins;
+      const uint32_t* xh = p.seq[si].xhist + ((size_t)xunit * P * G + g) * kHistBins;  // + pc' * G * bins
       const int b = tid;  // one bin per consumer thread (kConsumers >= kHistBins)
-      int tot = 0;
-      if (b < kHistBins)
-        for (int r = 0; r < C; ++r) tot += hs[(size_t)r * kHistBins + b];
-      int c, unused0, tot_all, unused1;
-      head_scan2<1>(tot, 0, c, unused0, tot_all, unused1, scratch);
-      if (b < kHistBins && c < k_eff && c + tot >= k_eff) { owner_sc[0] = b; owner_sc[1] = c; }
+      int tot = 0, pre = 0;  // all ranks of the unit / clusters before this one (P > 1)
+      if (b < kHistBins) {
+        if (P > 1) {
+          for (int c2 = 0; c2 < P; ++c2) {
+            const int v = (int)__ldcg(xh + (size_t)c2 * G * kHistBins + b);
+            tot += v;
+            pre += c2 < pc ? v : 0;
+          }
+        } else {
+          for (int r = 0; r < C; ++r) tot += hs[(size_t)r * kHistBins + b];
+        }
+      }
+      int c, cp, tot_all, unused1;
+      head_scan2<1>(tot, pre, c, cp, tot_all, unused1, scratch);
+      if (b < kHistBins && c < k_eff && c + tot >= k_eff) {
+        owner_sc[0] = b;  // T
+        owner_sc[1] = c;  // below T over the unit
+        cl_cnt[0] = cp;   // below T in earlier clusters
+        cl_cnt[1] = pre;  // == T in earlier clusters
+      }
       consumer_sync();
       const int T = owner_sc[0];
       if (warp < C) {  // warp r: rank r's count below T and at T
@@ -493,7 +563,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       }
       consumer_sync();
       if (tid < C) {  // push (T, below, pre_lt, pre_eq) into rank tid's sc[g]
-        int pl = 0, pe = 0;
+        int pl = P > 1 ? cl_cnt[0] : 0, pe = P > 1 ? cl_cnt[1] : 0;
         for (int r = 0; r < tid; ++r) { pl += rank_cnt[r][0]; pe += rank_cnt[r][1]; }
         st_async_v4(mapa_shared(smem_addr(&sc[g][0]), (uint32_t)tid), (uint32_t)T, (uint32_t)owner_sc[1], (uint32_t)pl,
                     (uint32_t)pe, mapa_shared(smem_addr(sc_bar), (uint32_t)tid));
@@ -567,11 +637,11 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         }
       }
     }
-    if (rank == 0 && p.idx && t_in == 0) {  // estimator.cpp:80 caps the selection at S
+    if (gr == 0 && p.idx && t_in == 0) {  // estimator.cpp:80 caps the selection at S
       int32_t* row = p.idx + ((int64_t)si * n_q + q0 + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
     }
-    if (rank == 0 && p.cand && t_in == 0) {
+    if (gr == 0 && p.cand && t_in == 0) {
       uint32_t* row = p.cand + ((int64_t)si * n_q + q0 + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = 0xffffffffu;
     }
@@ -698,9 +768,44 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       const float4 v4 = *reinterpret_cast<const float4*>(q2 + 4 + lane * 4);
       acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
     }
+    if (P > 1) {  // this cluster's partial of head g -> global (merged by cluster 0 below)
+      float* xp = p.seq[si].xpart + (((size_t)xunit * P + pc) * G + g) * kPartStride;
+      if (lane == 0) { __stcg(xp, Lsum > 0.f ? M : -INFINITY); __stcg(xp + 1, Lsum); }
+      __stcg(reinterpret_cast<float4*>(xp + 4 + lane * 4), make_float4(acc[0], acc[1], acc[2], acc[3]));
+      continue;
+    }
     const float inv = 1.f / Lsum;
     float* op = p.out + ((int64_t)si * n_q + q0 + g) * kHeadDim + lane * 4;
     *reinterpret_cast<float4*>(op) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+  }
+  if (P > 1 && n_owned) {
+    consumer_sync();
+    if (tid == 0) unit_barrier(p.seq[si].xsync + xunit * 4 + 2, P * owners, pc == 0, p.status);
+    consumer_sync();
+    if (pc == 0) {
+      for (int g = warp; g < G; g += kConsumerWarps) {
+        if (g % C != rank) continue;
+        const float* xp = p.seq[si].xpart + ((size_t)xunit * P * G + g) * kPartStride;
+        float M = -INFINITY;
+        for (int c2 = 0; c2 < P; ++c2) {
+          const float* q2 = xp + (size_t)c2 * G * kPartStride;
+          if (__ldcg(q2 + 1) > 0.f) M = fmaxf(M, __ldcg(q2));
+        }
+        float Lsum = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c2 = 0; c2 < P; ++c2) {
+          const float* q2 = xp + (size_t)c2 * G * kPartStride;
+          const float l2 = __ldcg(q2 + 1);
+          if (!(l2 > 0.f)) continue;
+          const float c = exp2f(__ldcg(q2) - M);
+          Lsum += l2 * c;
+          const float4 v4 = __ldcg(reinterpret_cast<const float4*>(q2 + 4 + lane * 4));
+          acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
+        }
+        const float inv = 1.f / Lsum;
+        float* op = p.out + ((int64_t)si * n_q + q0 + g) * kHeadDim + lane * 4;
+        *reinterpret_cast<float4*>(op) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      }
+    }
   }
   ADAMAS_TRACE(11);
   if (p.trace != nullptr && tid == kTraceTid && !(p.dbg & 32)) p.trace[blockIdx.x * 16 + 15] = trace_clock(p.dbg);

@@ -310,3 +310,21 @@ def test_seq_shard_empty_rank_and_errors(gpu, oracle):
         ops.select_attend(c, q, torch.stack([keys] * 2).repeat(1, 1, 300)[:, :, :4800], 4800, 10, 0)
     part, gidx = ops.select_attend(c, q, g, 16, 1, 0, want_idx=True)  # nothing selected here
     assert (gidx.cpu().numpy() == -1).all() and (part[:, 1].cpu().numpy() == 0).all()
+
+
+@pytest.mark.parametrize("P,C,n_kv,G,steps", [(2, 4, 1, 1, 3), (4, 4, 2, 4, 2), (4, 2, 1, 2, 2), (8, 4, 1, 8, 1)])
+def test_fused_decode_multi_cluster_units(gpu, oracle, monkeypatch, P, C, n_kv, G, steps):
+    """A unit spanning P clusters: histograms and partials through global
+    memory with the self-resetting barrier (reused across consecutive steps)."""
+    monkeypatch.setenv("ADAMAS_P", str(P))
+    monkeypatch.setenv("ADAMAS_CLUSTER", str(C))
+    monkeypatch.setenv("ADAMAS_REQUIRE_FUSED", "1")
+    cache = run_decode(gpu, oracle, 12000, n_kv, G, 128, True, seed=P * 10 + G, steps=steps)
+    assert cache.status() == 0  # no barrier timeout
+
+
+def test_seq_shard_candidates_multi_cluster(gpu, oracle, monkeypatch):
+    monkeypatch.setenv("ADAMAS_P", "4")
+    monkeypatch.setenv("ADAMAS_CLUSTER", "4")
+    from tests.test_gpu_seqshard import test_seq_sharded_decode_matches_single_device as t
+    t(gpu, oracle, 20000, 2, 2, 4, 128, True)
