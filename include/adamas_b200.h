@@ -198,6 +198,67 @@ int adamas_seq_select_attend(const adamas_cache* cache, const void* q, int n_q_h
  * out float32 [n_q][128]. */
 int adamas_lse_merge(const float* partials, int n_ranks, int n_q_heads, float* out, void* stream);
 
+/* ---------------------------------------------------------------- f3: harness selection backend
+ * The sweep harness's selection step on the GPU, in the
+ * harness's own arithmetic: fp64 inputs, any power-of-two head_dim in
+ * [2, 1024], 1/2/3-bit codes, with or without the Hadamard transform. Codes,
+ * distances, dot and page scores are bit-identical to the reference's (same
+ * correctly rounded fp64 operations in the same order); the selections are
+ * therefore identical index sets.
+ *
+ * Rows and instances: the harness pairs every query with one key/value
+ * instance (workload.hpp:69-80). Gaussian workloads share one instance across
+ * all queries, planted-needle workloads own one per query. Inputs are stacked
+ * device arrays keys/values [n_inst][seq_len][head_dim], queries
+ * [n_rows][head_dim]; row r reads instance r / rows_per_inst.
+ * Index outputs are int64 [n_rows][budget], ascending, -1 past the selection. */
+typedef struct adamas_hsel adamas_hsel;
+
+/* PolicySpec{adamas, bits, metric, with_hadamard} (sweep.hpp:15-33). Rejects
+ * head_dim outside {2, 4, ..., 1024} and bits outside 1..3 (quantizer.cpp:17-21). */
+int adamas_hsel_create(adamas_hsel** out, int head_dim, int bits, int with_hadamard);
+int adamas_hsel_destroy(adamas_hsel* sel);
+
+/* build_cache (sweep.cpp:38-50) over n_inst key matrices: encode (sweep.cpp:32-36)
+ * = fwht (hadamard.cpp:36-41) + compute_thresholds + bucketize (quantizer.cpp:40-85).
+ * Synchronises `stream`; a zero or non-finite key returns ADAMAS_ERR_CONFIG with
+ * the reference's message (quantizer.cpp:46-47). Replaces the previous build. */
+int adamas_hsel_build(adamas_hsel* sel, const double* keys, int64_t n_inst, int64_t seq_len, void* stream);
+
+/* Codes of built vectors first..first+n-1 (instance-major) in the reference's
+ * formats, device out: PackedCodes words (quantizer.cpp:87-117) for 1/2 bits
+ * (ceil(head_dim / (16 / bits)) uint16 per vector), CodeVector bytes for 3. */
+int adamas_hsel_codes_ref(const adamas_hsel* sel, int64_t first, int64_t n, void* out, void* stream);
+
+/* The adamas branch of select (sweep.cpp:87-98): encode each query, score_all
+ * (estimator.cpp:45-73, metric ADAMAS_METRIC_MANHATTAN or _EUCLIDEAN_SQ; the
+ * 1-bit pipeline uses popcount for both, estimator.cpp:51-52), top_k
+ * (estimator.cpp:75-90). Synchronises `stream` after encoding the queries
+ * (degenerate query -> ADAMAS_ERR_CONFIG). At most 65535 rows per call. */
+int adamas_hsel_select(adamas_hsel* sel, const double* queries, int64_t n_rows, int64_t rows_per_inst, int metric,
+                       int64_t budget, int64_t* idx, void* stream);
+
+/* The oracle policy / recall reference: top_k_by_score (baselines.cpp:21-32)
+ * over dot(q, k_i) (common.hpp:65-69), largest first, ties toward the smaller
+ * index. `scores` (nullable) receives the fp64 dot scores [n_rows][seq_len]. */
+int adamas_dot_topk(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst, int64_t n_inst,
+                    int64_t seq_len, int head_dim, int64_t k, int64_t* idx, double* scores, void* stream);
+
+/* The quest baseline: PageSummaries (baselines.cpp:34-54) + page_select
+ * (baselines.cpp:71-91). counts[r] = indices written for row r (the last page
+ * may be partial). budget must be a multiple of page_size unless >= seq_len. */
+int adamas_page_select(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst,
+                       int64_t n_inst, int64_t seq_len, int head_dim, int64_t page_size, int64_t budget, int64_t* idx,
+                       int64_t* counts, void* stream);
+
+/* full_attention (attention.cpp:8-38) in fp64 over all seq_len rows (idx NULL)
+ * or over the selected rows idx[r][0..counts[r]) (attend_subset, sweep.cpp:120-131;
+ * counts NULL = idx_stride rows each). out [n_rows][head_dim]. Same operation
+ * order as the reference; exp() may differ from libm's in the last place. */
+int adamas_attention_f64(const double* queries, const double* keys, const double* values, int64_t n_rows,
+                         int64_t rows_per_inst, int64_t n_inst, int64_t seq_len, int head_dim, const int64_t* idx,
+                         int64_t idx_stride, const int64_t* counts, double* out, void* stream);
+
 /* ---------------------------------------------------------------- diagnostics
  * Subsequent fused decode launches write up to 16 %globaltimer stamps per CTA
  * (phase boundaries) into device_buffer[blockIdx * 16 + i]; NULL disables. */

@@ -239,6 +239,115 @@ class Reference:
         L.ref_load_snapshot.restype = C.c_void_p
         L.ref_cache_rows.argtypes = [C.c_void_p, _SZ, C.POINTER(_D), C.POINTER(_D)]
         L.ref_cache_code_words.argtypes = [C.c_void_p, _SZ, C.POINTER(C.c_uint16)]
+        vp = C.c_void_p
+        spec_t = [C.c_uint64, _SZ, _SZ, _SZ, C.c_int, _D, _D, _SZ, _D]
+        L.ref_workload_instance.argtypes = spec_t + [_SZ, vp, vp, vp, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
+        L.ref_run_sweep.argtypes = spec_t + [vp, _SZ, vp, vp, vp, vp, vp, vp, _SZ, C.c_int,
+                                             C.c_char_p, _SZ, C.POINTER(_SZ), C.c_char_p, _SZ, C.POINTER(_SZ),
+                                             C.c_char_p, _SZ, C.POINTER(_SZ)]
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_rows_to_csv.argtypes = [vp, vp, vp, _SZ, C.c_char_p, _SZ]
+        L.ref_rows_to_csv.restype = _SZ
+        L.ref_top_k_by_score.argtypes = [vp, _SZ, _SZ, vp]
+        L.ref_top_k_by_score.restype = _SZ
+        L.ref_page_select.argtypes = [vp, vp, _SZ, _SZ, _SZ, _SZ, vp, C.POINTER(_SZ)]
+        L.ref_adamas_select.argtypes = [vp, vp, _SZ, _SZ, C.c_int, C.c_int, C.c_int, _SZ, vp, C.POINTER(_SZ), vp, vp]
+
+    # -- sweep harness (workload.cpp, sweep.cpp, baselines.cpp) -------------------
+    _KINDS = {"adamas": 0, "window": 1, "quest": 2, "oracle": 3}
+    _DISTS = {"gaussian": 0, "gaussian_with_outliers": 1, "planted_needle": 2}
+
+    @classmethod
+    def _spec_args(cls, w):
+        return [w.seed, w.seq_len, w.head_dim, w.num_queries, cls._DISTS[w.distribution], w.outlier_frac,
+                w.outlier_scale, w.position, w.snr]
+
+    def workload_instance(self, w, qi):
+        """Workload(w).instance(qi) (workload.cpp:125-155) -> (seed, query, keys, values, needle or None)."""
+        q = np.zeros(w.head_dim)
+        K = np.zeros((w.seq_len, w.head_dim))
+        V = np.zeros((w.seq_len, w.head_dim))
+        seed = C.c_uint64(0)
+        needle = C.c_int64(-1)
+        rc = self.L.ref_workload_instance(*self._spec_args(w), qi, q.ctypes.data, K.ctypes.data, V.ctypes.data,
+                                          C.byref(seed), C.byref(needle))
+        if rc:
+            raise ValueError("ConfigError: workload")
+        return seed.value, q, K, V, (None if needle.value < 0 else needle.value)
+
+    def run_sweep(self, w, sweep):
+        """run_sweep (sweep.cpp:189-253) -> (rows CSV, rows JSON, needle summary CSV or None)."""
+        pol = sweep.policies
+        budgets = np.array(sweep.budgets, dtype=np.uint64)
+        kinds = np.array([self._KINDS[p.kind] for p in pol], np.int32)
+        bits = np.array([p.bits for p in pol], np.int32)
+        metrics = np.array([0 if p.metric in ("l1", "manhattan") else 1 for p in pol], np.int32)
+        had = np.array([int(p.with_hadamard) for p in pol], np.int32)
+        sinks = np.array([p.sink for p in pol], np.uint64)
+        pages = np.array([p.page_size for p in pol], np.uint64)
+        cap = 1 << 16
+        while True:
+            bufs = [C.create_string_buffer(cap) for _ in range(3)]
+            lens = [_SZ(0) for _ in range(3)]
+            rc = self.L.ref_run_sweep(*self._spec_args(w), budgets.ctypes.data, budgets.size, kinds.ctypes.data,
+                                      bits.ctypes.data, metrics.ctypes.data, had.ctypes.data, sinks.ctypes.data,
+                                      pages.ctypes.data, len(pol), int(sweep.measure_output_error),
+                                      bufs[0], cap, C.byref(lens[0]), bufs[1], cap, C.byref(lens[1]),
+                                      bufs[2], cap, C.byref(lens[2]))
+            if rc:
+                raise (ValueError if rc == 1 else RuntimeError)(self.L.ref_last_error().decode())
+            if max(x.value for x in lens) < cap:
+                break
+            cap = max(x.value for x in lens) + 1
+        csv, js, nd = (b.value.decode() for b in bufs)
+        return csv, js, (nd if lens[2].value else None)
+
+    def rows_to_csv(self, recall, output_error=None):
+        """rows_to_csv over rows carrying these recall / output_error values."""
+        r = np.ascontiguousarray(recall, dtype=np.float64)
+        e = np.zeros_like(r) if output_error is None else np.ascontiguousarray(output_error, dtype=np.float64)
+        has = np.full(r.size, 0 if output_error is None else 1, np.int32)
+        n = self.L.ref_rows_to_csv(r.ctypes.data, e.ctypes.data, has.ctypes.data, r.size, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        self.L.ref_rows_to_csv(r.ctypes.data, e.ctypes.data, has.ctypes.data, r.size, buf, n + 1)
+        return buf.value.decode()
+
+    def top_k_by_score(self, scores, k):
+        s = np.ascontiguousarray(scores, dtype=np.float64)
+        out = np.zeros(min(k, s.size), np.int64)
+        n = self.L.ref_top_k_by_score(s.ctypes.data, s.size, k, out.ctypes.data)
+        return out[:n]
+
+    def page_select(self, q, K, page_size, k):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        out = np.zeros(max(k, K.shape[0]), np.int64)
+        n = _SZ(0)
+        rc = self.L.ref_page_select(q.ctypes.data, K.ctypes.data, K.shape[0], K.shape[1], page_size, k,
+                                    out.ctypes.data, C.byref(n))
+        if rc:
+            raise ValueError("ConfigError: page_select: " + self.L.ref_last_error().decode())
+        return out[:n.value]
+
+    def adamas_select(self, q, K, bits, metric, with_hadamard, k, want_codes=False):
+        """select's adamas branch (sweep.cpp:87-98) -> indices (and key / query codes in
+        the reference formats when want_codes)."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        S, d = K.shape
+        cb = d if bits == 3 else 2 * ((d + 16 // bits - 1) // (16 // bits))
+        kc = np.zeros((S, cb), np.uint8) if want_codes else None
+        qc = np.zeros(cb, np.uint8) if want_codes else None
+        out = np.zeros(max(min(k, S), 1), np.int64)
+        n = _SZ(0)
+        rc = self.L.ref_adamas_select(q.ctypes.data, K.ctypes.data, S, d, bits, metric, int(with_hadamard), k,
+                                      out.ctypes.data, C.byref(n), None if kc is None else kc.ctypes.data,
+                                      None if qc is None else qc.ctypes.data)
+        if rc:
+            raise ValueError("ConfigError: adamas_select: " + self.L.ref_last_error().decode())
+        if want_codes:
+            return out[:n.value], kc, qc
+        return out[:n.value]
 
     # -- ablation metrics (estimator.cpp:45-59, kernels.hpp:24-32) ---------------
     def encode_pack_bits(self, x, bits):

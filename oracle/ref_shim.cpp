@@ -11,6 +11,7 @@
 #include <exception>
 #include <memory>
 #include <numeric>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -21,20 +22,27 @@
 #include "adamas/kv_cache.hpp"
 #include "adamas/quantizer.hpp"
 #include "adamas/simd.hpp"
+#include "adamas/baselines.hpp"
+#include "adamas/sweep.hpp"
+#include "adamas/workload.hpp"
 
 using namespace adamas;
 
 namespace {
 
 // 0 ok, 1 ConfigError, 2 any other std::exception (adamas_cli.cpp:233-243 mapping).
+thread_local std::string g_error;
+
 template <typename F>
 int guarded(F&& f) {
   try {
     f();
     return 0;
-  } catch (const ConfigError&) {
+  } catch (const ConfigError& e) {
+    g_error = e.what();
     return 1;
-  } catch (const std::exception&) {
+  } catch (const std::exception& e) {
+    g_error = e.what();
     return 2;
   }
 }
@@ -69,9 +77,175 @@ float round_bf16(float x) {
   return y;
 }
 
+WorkloadSpec make_spec(uint64_t seed, size_t seq_len, size_t head_dim, size_t num_queries, int distribution,
+                       double outlier_frac, double outlier_scale, size_t position, double snr) {
+  WorkloadSpec w;
+  w.seed = seed;
+  w.seq_len = seq_len;
+  w.head_dim = head_dim;
+  w.num_queries = num_queries;
+  w.distribution = static_cast<DistributionKind>(distribution);
+  w.outlier_frac = outlier_frac;
+  w.outlier_scale = outlier_scale;
+  w.position = position;
+  w.snr = snr;
+  return w;
+}
+
+// kinds: 0 adamas, 1 window, 2 quest, 3 oracle (PolicySpec::Kind order); metric 0 l1, 1 l2.
+SweepConfig make_sweep(const size_t* budgets, size_t n_budgets, const int* kinds, const int* bits,
+                       const int* metrics, const int* hadamard, const size_t* sinks, const size_t* page_sizes,
+                       size_t n_policies, int measure_output_error) {
+  SweepConfig c;
+  c.budgets.assign(budgets, budgets + n_budgets);
+  for (size_t i = 0; i < n_policies; ++i) {
+    PolicySpec p;
+    p.kind = static_cast<PolicySpec::Kind>(kinds[i]);
+    p.bits = bits[i];
+    p.metric = metrics[i] == 0 ? Metric::manhattan : Metric::euclidean_sq;
+    p.with_hadamard = hadamard[i] != 0;
+    p.sink = sinks[i];
+    p.page_size = page_sizes[i];
+    c.policies.push_back(p);
+  }
+  c.measure_output_error = measure_output_error != 0;
+  return c;
+}
+
+size_t put(const std::string& text, char* out, size_t cap) {
+  if (out && cap > 0) {
+    const size_t n = std::min(cap - 1, text.size());
+    std::memcpy(out, text.data(), n);
+    out[n] = 0;
+  }
+  return text.size();
+}
+
 }  // namespace
 
 extern "C" {
+
+// Workload::instance (workload.cpp:125-155): writes query [d], keys and values
+// [seq_len][d], the instance seed and the needle position (-1 if none).
+int ref_workload_instance(uint64_t seed, size_t seq_len, size_t head_dim, size_t num_queries, int distribution,
+                          double outlier_frac, double outlier_scale, size_t position, double snr, size_t qi,
+                          double* query, double* keys, double* values, uint64_t* inst_seed, int64_t* needle) {
+  return guarded([&] {
+    const Workload w(make_spec(seed, seq_len, head_dim, num_queries, distribution, outlier_frac, outlier_scale,
+                               position, snr));
+    const WorkloadInstance inst = w.instance(qi);
+    std::copy(inst.query.begin(), inst.query.end(), query);
+    std::copy(inst.keys->data().begin(), inst.keys->data().end(), keys);
+    std::copy(inst.values->data().begin(), inst.values->data().end(), values);
+    *inst_seed = inst.seed;
+    *needle = inst.needle_position ? (int64_t)*inst.needle_position : -1;
+  });
+}
+
+// run_sweep (sweep.cpp:189-253) + rows_to_csv / rows_to_json (:280-318); the
+// needle summary CSV (:255-272, :320-334) when the workload plants needles.
+// Each text is returned through (out, cap) with its full length; rc as guarded
+// (the ConfigError text via ref_last_error).
+int ref_run_sweep(uint64_t seed, size_t seq_len, size_t head_dim, size_t num_queries, int distribution,
+                  double outlier_frac, double outlier_scale, size_t position, double snr, const size_t* budgets,
+                  size_t n_budgets, const int* kinds, const int* bits, const int* metrics, const int* hadamard,
+                  const size_t* sinks, const size_t* page_sizes, size_t n_policies, int measure_output_error,
+                  char* csv, size_t csv_cap, size_t* csv_len, char* json, size_t json_cap, size_t* json_len,
+                  char* needle_csv, size_t needle_cap, size_t* needle_len) {
+  try {
+    const auto rows = run_sweep(make_spec(seed, seq_len, head_dim, num_queries, distribution, outlier_frac,
+                                          outlier_scale, position, snr),
+                                make_sweep(budgets, n_budgets, kinds, bits, metrics, hadamard, sinks, page_sizes,
+                                           n_policies, measure_output_error));
+    *csv_len = put(rows_to_csv(rows), csv, csv_cap);
+    *json_len = put(rows_to_json(rows), json, json_cap);
+    *needle_len = 0;
+    if (!rows.empty() && rows[0].needle_hit) *needle_len = put(needle_summary_to_csv(needle_report(rows)), needle_csv, needle_cap);
+    return 0;
+  } catch (const ConfigError& e) {
+    g_error = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return 2;
+  }
+}
+
+const char* ref_last_error() { return g_error.c_str(); }
+
+// rows_to_csv over caller-made rows (sweep.cpp:280-297): pins format_number
+// (the JSON library's shortest round-trip double text) on arbitrary values.
+size_t ref_rows_to_csv(const double* recall, const double* output_error, const int* has_error, size_t n, char* out,
+                       size_t cap) {
+  std::vector<ResultRow> rows(n);
+  for (size_t i = 0; i < n; ++i) {
+    rows[i].policy = "p";
+    rows[i].recall = recall[i];
+    if (has_error[i]) rows[i].output_error = output_error[i];
+  }
+  return put(rows_to_csv(rows), out, cap);
+}
+
+// top_k_by_score (baselines.cpp:21-32) and page_select over PageSummaries
+// (baselines.cpp:34-91) for one query.
+size_t ref_top_k_by_score(const double* scores, size_t n, size_t k, int64_t* idx) {
+  const auto sel = top_k_by_score(std::span<const double>(scores, n), k);
+  for (size_t i = 0; i < sel.size(); ++i) idx[i] = (int64_t)sel[i];
+  return sel.size();
+}
+
+int ref_page_select(const double* q, const double* keys, size_t seq_len, size_t d, size_t page_size, size_t k,
+                    int64_t* idx, size_t* n_out) {
+  return guarded([&] {
+    PageSummaries pages(page_size, d);
+    for (size_t i = 0; i < seq_len; ++i) pages.append(std::span<const double>(keys + i * d, d));
+    const auto sel = page_select(std::span<const double>(q, d), pages, k);
+    for (size_t i = 0; i < sel.indices.size(); ++i) idx[i] = (int64_t)sel.indices[i];
+    *n_out = sel.indices.size();
+  });
+}
+
+// The adamas branch of select (sweep.cpp:87-98) for one query against keys
+// [seq_len][d]: build_cache (sweep.cpp:38-50), encode, score_all, top_k.
+int ref_adamas_select(const double* q, const double* keys, size_t seq_len, size_t d, int bits, int metric,
+                      int hadamard, size_t k, int64_t* idx, size_t* n_out, uint8_t* key_codes, uint8_t* q_codes) {
+  return guarded([&] {
+    auto enc = [&](std::span<const double> x) {
+      if (!hadamard) return bucketize(x, compute_thresholds(x, bits));
+      const RealVector t = fwht(x, {.dim = x.size()});
+      return bucketize(t, compute_thresholds(t, bits));
+    };
+    const Metric m = metric == 0 ? Metric::manhattan : Metric::euclidean_sq;
+    KvCache cache(d, bits);
+    const std::vector<double> zero(d, 0.0);
+    const size_t cb = packed_bytes(d, bits);
+    for (size_t i = 0; i < seq_len; ++i) {
+      const std::span<const double> row(keys + i * d, d);
+      const CodeVector c = enc(row);
+      if (bits == 3) {
+        cache.update(row, zero, c);
+        if (key_codes) std::copy(c.codes.begin(), c.codes.end(), key_codes + i * cb);
+      } else {
+        const PackedCodes p = pack(c);
+        cache.update(row, zero, p);
+        if (key_codes) std::memcpy(key_codes + i * cb, p.words.data(), p.words.size() * 2);
+      }
+    }
+    const CodeVector qc = enc(std::span<const double>(q, d));
+    DistanceScores scores;
+    if (bits == 3) {
+      scores = score_all(qc, cache, m);
+      if (q_codes) std::copy(qc.codes.begin(), qc.codes.end(), q_codes);
+    } else {
+      const PackedCodes qp = pack(qc);
+      scores = score_all(qp, cache, m);
+      if (q_codes) std::memcpy(q_codes, qp.words.data(), qp.words.size() * 2);
+    }
+    const auto sel = top_k(scores, k);
+    for (size_t i = 0; i < sel.indices.size(); ++i) idx[i] = (int64_t)sel.indices[i];
+    *n_out = sel.indices.size();
+  });
+}
 
 const char* ref_simd_level() { return simd_level_name(active_simd_level()); }
 

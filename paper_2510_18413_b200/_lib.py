@@ -25,7 +25,9 @@ EXPORTED = [
     "adamas_decode_step", "adamas_decode_step_batched", "adamas_codes_ref_to_planes",
     "adamas_codes_planes_to_ref", "adamas_debug_trace", "adamas_seq_local_candidates",
     "adamas_seq_select_attend", "adamas_lse_merge", "adamas_cache_save_adkv", "adamas_cache_load_adkv",
-    "adamas_score_metric",
+    "adamas_score_metric", "adamas_hsel_create", "adamas_hsel_destroy", "adamas_hsel_build",
+    "adamas_hsel_codes_ref", "adamas_hsel_select", "adamas_dot_topk", "adamas_page_select",
+    "adamas_attention_f64",
 ]
 
 
@@ -75,6 +77,14 @@ def load() -> C.CDLL:
     L.adamas_cache_save_adkv.argtypes = [vp, i32, C.c_char_p, vp]
     L.adamas_score_metric.argtypes = [vp, vp, i32, i32, vp, vp]
     L.adamas_cache_load_adkv.argtypes = [vp, C.POINTER(C.c_char_p), i32, vp]
+    L.adamas_hsel_create.argtypes = [C.POINTER(vp), i32, i32, i32]
+    L.adamas_hsel_destroy.argtypes = [vp]
+    L.adamas_hsel_build.argtypes = [vp, vp, i64, i64, vp]
+    L.adamas_hsel_codes_ref.argtypes = [vp, i64, i64, vp, vp]
+    L.adamas_hsel_select.argtypes = [vp, vp, i64, i64, i32, i64, vp, vp]
+    L.adamas_dot_topk.argtypes = [vp, vp, i64, i64, i64, i64, i32, i64, vp, vp, vp]
+    L.adamas_page_select.argtypes = [vp, vp, i64, i64, i64, i64, i32, i64, i64, vp, vp, vp]
+    L.adamas_attention_f64.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp, vp]
     for name in EXPORTED:
         if not hasattr(L, name):
             raise ImportError(f"{lib} does not export {name}")

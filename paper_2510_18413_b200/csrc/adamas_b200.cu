@@ -14,6 +14,7 @@
 #include "../../include/adamas_b200.h"
 #include "fused_decode.cuh"
 #include "ops.cuh"
+#include "harness_select.cuh"
 
 using namespace adamas_dev;
 
@@ -360,6 +361,99 @@ template <typename Tp>
 void put(std::ofstream& os, Tp v) { os.write(reinterpret_cast<const char*>(&v), sizeof(Tp)); }
 template <typename Tp>
 bool get(std::ifstream& is, Tp& v) { return (bool)is.read(reinterpret_cast<char*>(&v), sizeof(Tp)); }
+}  // namespace
+
+// ------------------------------------------------------------------ f3 harness selection
+// Device code store of build_cache for n_inst independent key matrices.
+struct adamas_hsel {
+  int head_dim = 0, bits = 0, hadamard = 1;
+  int64_t n_inst = 0, seq_len = 0;
+  uint32_t* planes = nullptr;  // [n_inst * seq_len][2][W] (bits 1, 2)
+  uint8_t* bytes = nullptr;    // [n_inst * seq_len][D] (bits 3)
+  size_t code_cap = 0;         // bytes allocated for the codes
+  void* qcodes = nullptr;      // encoded queries
+  size_t q_cap = 0;
+  uint32_t* scores = nullptr;
+  size_t scores_cap = 0;
+  int* status = nullptr;       // device status word (kHselZero | kHselNonFinite)
+};
+
+namespace {
+
+int grow_bytes(void** p, size_t* have, size_t need) {
+  if (*have >= need) return ADAMAS_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  ADAMAS_CUDA(cudaMalloc(p, need));
+  *have = need;
+  return ADAMAS_OK;
+}
+
+bool pow2_dim(int d) { return d >= 2 && d <= kHselMaxDim && (d & (d - 1)) == 0; }
+
+size_t hsel_code_bytes(int D, int bits) {
+  return bits == 3 ? (size_t)D : (size_t)2 * hsel_words(D) * sizeof(uint32_t);
+}
+
+int hsel_encode(int D, int bits, int hadamard, const double* x, int64_t n_vec, void* codes, int* status,
+                cudaStream_t s) {
+  if (n_vec == 0) return ADAMAS_OK;
+  const int grid = (int)std::min<int64_t>((n_vec + kHselWarps - 1) / kHselWarps, (int64_t)sm_count() * 16);
+  uint32_t* pl = bits == 3 ? nullptr : static_cast<uint32_t*>(codes);
+  uint8_t* by = bits == 3 ? static_cast<uint8_t*>(codes) : nullptr;
+#define HSEL_ENC(E_) hsel_encode_kernel<E_><<<grid, kHselWarps * 32, 0, s>>>(x, n_vec, D, bits, hadamard, pl, by, status)
+  switch (D >= 32 ? D / 32 : 1) {
+    case 1: HSEL_ENC(1); break;
+    case 2: HSEL_ENC(2); break;
+    case 4: HSEL_ENC(4); break;
+    case 8: HSEL_ENC(8); break;
+    case 16: HSEL_ENC(16); break;
+    case 32: HSEL_ENC(32); break;
+    default: return fail(ADAMAS_ERR_CONFIG, "hsel: unsupported head_dim");
+  }
+#undef HSEL_ENC
+  return launch_check("hsel_encode_kernel");
+}
+
+// Reads and clears the status word; the reference throws ConfigError from
+// compute_thresholds for the first bad vector (quantizer.cpp:46-47).
+int hsel_status_check(int* status, cudaStream_t s) {
+  int h = 0;
+  ADAMAS_CUDA(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  ADAMAS_CUDA(cudaStreamSynchronize(s));
+  if (h == 0) return ADAMAS_OK;
+  ADAMAS_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+  if (h & kHselNonFinite) return fail(ADAMAS_ERR_CONFIG, "non-finite input to compute_thresholds");
+  return fail(ADAMAS_ERR_CONFIG, "degenerate scale: input vector is all zeros");
+}
+
+int check_rows(int64_t n_rows, int64_t rows_per_inst, int64_t n_inst) {
+  if (n_rows < 0 || rows_per_inst < 1) return fail(ADAMAS_ERR_CONFIG, "rows: bad row count / rows_per_inst");
+  if (n_rows > 0 && (n_rows - 1) / rows_per_inst >= n_inst)
+    return fail(ADAMAS_ERR_CONFIG, "rows: more query rows than instances * rows_per_inst");
+  return ADAMAS_OK;
+}
+
+int topk_launch(int mode, const void* scores, int64_t n_rows, int64_t n, int64_t k, int64_t* idx, cudaStream_t s) {
+  if (n_rows == 0) return ADAMAS_OK;
+  if (n_rows > 0x7fffffff) return fail(ADAMAS_ERR_CONFIG, "topk: too many rows");
+  if (mode == 0)
+    hsel_topk_kernel<0><<<(unsigned)n_rows, kHselTopkThreads, 0, s>>>(scores, n, k, idx);
+  else
+    hsel_topk_kernel<1><<<(unsigned)n_rows, kHselTopkThreads, 0, s>>>(scores, n, k, idx);
+  return launch_check("hsel_topk_kernel");
+}
+
+int dot_scores(const double* q, const double* keys, int64_t n_rows, int64_t rows_per_inst, int64_t S, int D,
+               double* out, cudaStream_t s) {
+  if (n_rows == 0 || S == 0) return ADAMAS_OK;
+  if (n_rows > 65535) return fail(ADAMAS_ERR_CONFIG, "dot: at most 65535 query rows per call");
+  const dim3 grid((unsigned)((S + kHselDotTok - 1) / kHselDotTok), (unsigned)n_rows);
+  hsel_dot_kernel<<<grid, kHselDotTok, 0, s>>>(q, keys, S, D, rows_per_inst, out);
+  return launch_check("hsel_dot_kernel");
+}
+
 }  // namespace
 
 extern "C" {
@@ -810,4 +904,182 @@ void adamas_codes_planes_to_ref(const uint32_t* planes, int64_t n, uint16_t* ref
   }
 }
 
+// ------------------------------------------------------------------ f3 harness selection
+int adamas_hsel_create(adamas_hsel** out, int head_dim, int bits, int with_hadamard) {
+  if (!out) return fail(ADAMAS_ERR_CONFIG, "hsel_create: null out");
+  *out = nullptr;
+  if (!pow2_dim(head_dim))
+    return fail(ADAMAS_ERR_CONFIG, "hsel: head_dim must be a power of two in [2, 1024], got " +
+                                       std::to_string(head_dim));
+  if (bits < 1 || bits > 3)
+    return fail(ADAMAS_ERR_CONFIG, "bucketization width must be 1, 2, or 3 bits, got " + std::to_string(bits));
+  auto* h = new adamas_hsel();
+  h->head_dim = head_dim;
+  h->bits = bits;
+  h->hadamard = with_hadamard ? 1 : 0;
+  if (cudaMalloc(&h->status, sizeof(int)) != cudaSuccess || cudaMemset(h->status, 0, sizeof(int)) != cudaSuccess) {
+    delete h;
+    return fail(ADAMAS_ERR_RUNTIME, "hsel_create: cudaMalloc failed");
+  }
+  *out = h;
+  return ADAMAS_OK;
+}
+
+int adamas_hsel_destroy(adamas_hsel* h) {
+  if (!h) return ADAMAS_OK;
+  cudaFree(h->planes);
+  cudaFree(h->bytes);
+  cudaFree(h->qcodes);
+  cudaFree(h->scores);
+  cudaFree(h->status);
+  delete h;
+  return ADAMAS_OK;
+}
+
+int adamas_hsel_build(adamas_hsel* h, const double* keys, int64_t n_inst, int64_t seq_len, void* stream) {
+  if (!h) return fail(ADAMAS_ERR_CONFIG, "null hsel handle");
+  if (n_inst < 0 || seq_len < 0) return fail(ADAMAS_ERR_CONFIG, "hsel_build: negative size");
+  if (n_inst * seq_len > 0 && !keys) return fail(ADAMAS_ERR_CONFIG, "hsel_build: null keys");
+  cudaStream_t s = as_stream(stream);
+  const int64_t n_vec = n_inst * seq_len;
+  const size_t need = std::max<size_t>(1, (size_t)n_vec * hsel_code_bytes(h->head_dim, h->bits));
+  void** buf = h->bits == 3 ? reinterpret_cast<void**>(&h->bytes) : reinterpret_cast<void**>(&h->planes);
+  if (int rc = grow_bytes(buf, &h->code_cap, need)) return rc;
+  h->n_inst = n_inst;
+  h->seq_len = seq_len;
+  if (int rc = hsel_encode(h->head_dim, h->bits, h->hadamard, keys, n_vec, *buf, h->status, s)) return rc;
+  return hsel_status_check(h->status, s);
+}
+
+int adamas_hsel_codes_ref(const adamas_hsel* h, int64_t first, int64_t n, void* out, void* stream) {
+  if (!h) return fail(ADAMAS_ERR_CONFIG, "null hsel handle");
+  if (first < 0 || n < 0 || first + n > h->n_inst * h->seq_len)
+    return fail(ADAMAS_ERR_CONFIG, "hsel_codes_ref: range out of bounds");
+  if (n == 0) return ADAMAS_OK;
+  const int W = hsel_words(h->head_dim);
+  const int grid = (int)std::min<int64_t>((n * h->head_dim + 255) / 256, (int64_t)sm_count() * 8);
+  hsel_codes_ref_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      h->planes ? h->planes + first * 2 * W : nullptr, h->bytes ? h->bytes + first * h->head_dim : nullptr, n,
+      h->head_dim, h->bits, out);
+  return launch_check("hsel_codes_ref_kernel");
+}
+
+int adamas_hsel_select(adamas_hsel* h, const double* queries, int64_t n_rows, int64_t rows_per_inst, int metric,
+                       int64_t budget, int64_t* idx, void* stream) {
+  if (!h) return fail(ADAMAS_ERR_CONFIG, "null hsel handle");
+  if (metric != ADAMAS_METRIC_MANHATTAN && metric != ADAMAS_METRIC_EUCLIDEAN_SQ)
+    return fail(ADAMAS_ERR_CONFIG, "hsel_select: metric must be manhattan or euclidean_sq");
+  if (budget < 0) return fail(ADAMAS_ERR_CONFIG, "hsel_select: negative budget");
+  if (int rc = check_rows(n_rows, rows_per_inst, h->n_inst)) return rc;
+  if (n_rows == 0) return ADAMAS_OK;
+  if (n_rows > 65535) return fail(ADAMAS_ERR_CONFIG, "hsel_select: at most 65535 query rows per call");
+  if (!queries || (budget > 0 && !idx)) return fail(ADAMAS_ERR_CONFIG, "hsel_select: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int D = h->head_dim;
+  if (int rc = grow_bytes(&h->qcodes, &h->q_cap, (size_t)n_rows * hsel_code_bytes(D, h->bits))) return rc;
+  if (int rc = hsel_encode(D, h->bits, h->hadamard, queries, n_rows, h->qcodes, h->status, s)) return rc;
+  if (int rc = hsel_status_check(h->status, s)) return rc;
+  const int64_t S = h->seq_len;
+  if (budget == 0) return ADAMAS_OK;
+  if (S == 0) {
+    ADAMAS_CUDA(cudaMemsetAsync(idx, 0xff, (size_t)n_rows * budget * sizeof(int64_t), s));
+    return ADAMAS_OK;
+  }
+  void* sc = h->scores;
+  if (int rc = grow_bytes(&sc, &h->scores_cap, (size_t)n_rows * S * sizeof(uint32_t))) return rc;
+  h->scores = static_cast<uint32_t*>(sc);
+  const dim3 grid((unsigned)((S + kHselScoreThreads - 1) / kHselScoreThreads), (unsigned)n_rows);
+  const uint32_t* qp = h->bits == 3 ? nullptr : static_cast<const uint32_t*>(h->qcodes);
+  const uint8_t* qb = h->bits == 3 ? static_cast<const uint8_t*>(h->qcodes) : nullptr;
+#define HSEL_SCORE(B_, M_) \
+  hsel_score_kernel<B_, M_><<<grid, kHselScoreThreads, 0, s>>>(h->planes, h->bytes, qp, qb, S, D, rows_per_inst, h->scores)
+  const bool l1 = metric == ADAMAS_METRIC_MANHATTAN;
+  if (h->bits == 1) HSEL_SCORE(1, kMetricManhattan);
+  else if (h->bits == 2) { if (l1) HSEL_SCORE(2, kMetricManhattan); else HSEL_SCORE(2, kMetricEuclideanSq); }
+  else { if (l1) HSEL_SCORE(3, kMetricManhattan); else HSEL_SCORE(3, kMetricEuclideanSq); }
+#undef HSEL_SCORE
+  if (int rc = launch_check("hsel_score_kernel")) return rc;
+  return topk_launch(0, h->scores, n_rows, S, budget, idx, s);
+}
+
+int adamas_dot_topk(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst, int64_t n_inst,
+                    int64_t seq_len, int head_dim, int64_t k, int64_t* idx, double* scores, void* stream) {
+  if (head_dim < 1 || head_dim > kHselMaxDim) return fail(ADAMAS_ERR_CONFIG, "dot_topk: head_dim out of range");
+  if (k < 0 || seq_len < 0) return fail(ADAMAS_ERR_CONFIG, "dot_topk: negative size");
+  if (int rc = check_rows(n_rows, rows_per_inst, n_inst)) return rc;
+  if (n_rows == 0) return ADAMAS_OK;
+  cudaStream_t s = as_stream(stream);
+  double* sc = scores;
+  if (!sc) ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), std::max<size_t>(8, (size_t)n_rows * seq_len * 8), s));
+  int rc = dot_scores(queries, keys, n_rows, rows_per_inst, seq_len, head_dim, sc, s);
+  if (!rc && k > 0) rc = topk_launch(1, sc, n_rows, seq_len, k, idx, s);
+  if (!scores) cudaFreeAsync(sc, s);
+  return rc;
+}
+
+int adamas_page_select(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst,
+                       int64_t n_inst, int64_t seq_len, int head_dim, int64_t page_size, int64_t budget, int64_t* idx,
+                       int64_t* counts, void* stream) {
+  if (page_size < 1) return fail(ADAMAS_ERR_CONFIG, "PageSummaries: page_size must be positive");
+  if (head_dim < 1 || head_dim > kHselMaxDim) return fail(ADAMAS_ERR_CONFIG, "page_select: head_dim out of range");
+  if (budget < 0 || seq_len < 0) return fail(ADAMAS_ERR_CONFIG, "page_select: negative size");
+  if (int rc = check_rows(n_rows, rows_per_inst, n_inst)) return rc;
+  if (n_rows == 0 || budget == 0) return ADAMAS_OK;
+  cudaStream_t s = as_stream(stream);
+  if (n_rows > 0x7fffffff) return fail(ADAMAS_ERR_CONFIG, "page_select: too many rows");
+  if (budget >= seq_len) {  // baselines.cpp:74-78: everything
+    hsel_topk_kernel<0><<<(unsigned)n_rows, kHselTopkThreads, 0, s>>>(nullptr, seq_len, budget, idx);
+    if (int rc = launch_check("hsel_topk_kernel")) return rc;
+    hsel_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(counts, n_rows, seq_len);
+    return launch_check("hsel_fill_kernel");
+  }
+  if (budget % page_size != 0) return fail(ADAMAS_ERR_CONFIG, "page_select: budget must be a multiple of the page size");
+  const int64_t P = (seq_len + page_size - 1) / page_size, kp = budget / page_size;
+  double *mins = nullptr, *maxs = nullptr, *ps = nullptr;
+  int64_t* pages = nullptr;
+  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mins), (size_t)n_inst * P * head_dim * 8, s));
+  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&maxs), (size_t)n_inst * P * head_dim * 8, s));
+  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ps), (size_t)n_rows * P * 8, s));
+  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pages), (size_t)n_rows * kp * 8, s));
+  const int g1 = (int)std::min<int64_t>((n_inst * P * head_dim + 255) / 256, (int64_t)sm_count() * 16);
+  hsel_page_summary_kernel<<<std::max(g1, 1), 256, 0, s>>>(keys, n_inst, seq_len, head_dim, page_size, mins, maxs);
+  int rc = launch_check("hsel_page_summary_kernel");
+  if (!rc) {
+    const int g2 = (int)std::min<int64_t>((n_rows * P + 255) / 256, (int64_t)sm_count() * 16);
+    hsel_page_score_kernel<<<std::max(g2, 1), 256, 0, s>>>(queries, mins, maxs, n_rows, rows_per_inst, P, head_dim, ps);
+    rc = launch_check("hsel_page_score_kernel");
+  }
+  if (!rc) rc = topk_launch(1, ps, n_rows, P, kp, pages, s);
+  if (!rc) {
+    hsel_page_expand_kernel<<<(unsigned)n_rows, 256, 0, s>>>(pages, kp, seq_len, page_size, budget, idx, counts);
+    rc = launch_check("hsel_page_expand_kernel");
+  }
+  cudaFreeAsync(mins, s);
+  cudaFreeAsync(maxs, s);
+  cudaFreeAsync(ps, s);
+  cudaFreeAsync(pages, s);
+  return rc;
+}
+
+int adamas_attention_f64(const double* queries, const double* keys, const double* values, int64_t n_rows,
+                         int64_t rows_per_inst, int64_t n_inst, int64_t seq_len, int head_dim, const int64_t* idx,
+                         int64_t idx_stride, const int64_t* counts, double* out, void* stream) {
+  if (head_dim < 1 || head_dim > kHselMaxDim) return fail(ADAMAS_ERR_CONFIG, "attention_f64: head_dim out of range");
+  if (int rc = check_rows(n_rows, rows_per_inst, n_inst)) return rc;
+  if (n_rows == 0) return ADAMAS_OK;
+  if (seq_len < 1 || (idx && idx_stride < 1)) return fail(ADAMAS_ERR_CONFIG, "full_attention: no keys to attend over");
+  if (n_rows > 0x7fffffff) return fail(ADAMAS_ERR_CONFIG, "attention_f64: too many rows");
+  cudaStream_t s = as_stream(stream);
+  const int64_t n_max = idx ? idx_stride : seq_len;
+  double* lg = nullptr;
+  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lg), (size_t)n_rows * n_max * 8, s));
+  hsel_attention_kernel<<<(unsigned)n_rows, kHselAttnThreads, 0, s>>>(queries, keys, values, seq_len, head_dim,
+                                                                       rows_per_inst, idx, idx_stride, counts, lg,
+                                                                       n_max, out);
+  const int rc = launch_check("hsel_attention_kernel");
+  cudaFreeAsync(lg, s);
+  return rc;
+}
+
 }  // extern "C"
+
