@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="longchat", choices=sorted(CONFIGS),
+    ap.add_argument("--config", default="longchat", choices=sorted(CONFIGS) + ["harness_needle"],
                     help="BASELINE.json config: longchat (configs[1], the headline), llama128k (configs[2]), "
                          "batched16 (configs[3]), seqshard1m (configs[4], per-rank work of the 8-way split)")
     ap.add_argument("--heads", type=int, default=None)
@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=11)
     a = ap.parse_args()
-    for k, v in CONFIGS[a.config].items():
+    for k, v in CONFIGS.get(a.config, {}).items():
         if getattr(a, k) is None:
             setattr(a, k, v)
     return a
@@ -455,8 +455,176 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- f3: the sweep harness
+HARNESS_METRIC = "needle sweep us/query (adamas + window + quest x budgets 16/32/64 + recall reference)"
+HARNESS_UNIT = "us/query"
+HARNESS = dict(seq=8192, head_dim=128, queries=100, budgets=(16, 32, 64), position=4096, snr=10.0)
+
+
+def _harness_sweep(H):
+    return H.SweepConfig(budgets=list(HARNESS["budgets"]),
+                         policies=[H.PolicySpec("adamas"), H.PolicySpec("window", sink=4),
+                                   H.PolicySpec("quest", page_size=16)], measure_output_error=False)
+
+
+def harness_cpu_reference(n_queries):
+    """The reference's run_sweep (oracle/_ref) over the acceptance needle shape
+    (acceptance.cpp:290-325) on n_queries queries, minus its own workload
+    generation (timed separately through Workload::instance). Returns
+    (us per query, sample text)."""
+    from oracle.bindings import Reference
+    from paper_2510_18413_b200 import harness as H
+
+    ref = Reference()
+    spec = H.WorkloadSpec(seed=2024, seq_len=HARNESS["seq"], head_dim=HARNESS["head_dim"], num_queries=n_queries,
+                          distribution="planted_needle", position=HARNESS["position"], snr=HARNESS["snr"])
+    t0 = time.perf_counter()
+    ref.run_sweep(spec, _harness_sweep(H))
+    t_sweep = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for qi in range(n_queries):
+        ref.workload_instance(spec, qi)
+    t_gen = time.perf_counter() - t0
+    us = (t_sweep - t_gen) * 1e6 / n_queries
+    sample = (f"reference run_sweep, planted needle S={HARNESS['seq']} d={HARNESS['head_dim']}, {n_queries} queries "
+              f"x budgets {list(HARNESS['budgets'])} x adamas/window/quest, 1 thread: {t_sweep:.2f} s minus its "
+              f"workload generation {t_gen:.2f} s")
+    return us, sample
+
+
+def run_harness(args):
+    """f3: the sweep harness's per-query work on the GPU. One step = one sweep
+    over HARNESS['queries'] planted-needle instances (each its own 8K x 128 fp64
+    keys, 839 MB per step, > L2): build_cache, adamas select, quest select and
+    the dot-product recall reference for every budget. `value`: instances
+    resident in HBM; `e2e`: harness.run_sweep on host instances (H2D of keys,
+    values and queries, D2H of the selections, host-side rows)."""
+    import numpy as np
+    import torch
+
+    from paper_2510_18413_b200 import harness as H
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    S, d, nq, budgets = HARNESS["seq"], HARNESS["head_dim"], HARNESS["queries"], HARNESS["budgets"]
+    rng = np.random.default_rng(1234 + rank)
+    insts = []
+    for qi in range(nq):  # workload.cpp:136-152's planted needle, numpy RNG
+        q = rng.standard_normal(d)
+        K = rng.standard_normal((S, d))
+        K[HARNESS["position"]] = HARNESS["snr"] * np.sqrt(d) / np.linalg.norm(q) * q + rng.standard_normal(d)
+        insts.append(H.Instance(qi, q, K, rng.standard_normal((S, d)), HARNESS["position"]))
+    Kd = torch.empty((nq, S, d), dtype=torch.float64, device="cuda")
+    for i, x in enumerate(insts):
+        Kd[i].copy_(torch.from_numpy(x.keys))
+    Qd = torch.as_tensor(np.stack([x.query for x in insts]), device="cuda")
+    sel = H.HarnessSelector(d, 2, True)
+    pages = H.PageSelector(16, d)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    parts = {"build": [], "select": [], "quest": [], "recall": []}
+
+    def step(record):
+        marks = [ev() for _ in range(5)]
+        marks[0].record(stream)
+        sel.build(Kd)
+        marks[1].record(stream)
+        for b in budgets:
+            sel.select(Qd, b, "l1", 1)
+        marks[2].record(stream)
+        pages.build(Kd)
+        for b in budgets:
+            pages.select(Qd, b, 1)
+        marks[3].record(stream)
+        _, dots = H.dot_topk(Qd, Kd, 0, 1, want_scores=True)
+        for b in budgets:
+            H.topk_scores(dots, b)
+        marks[4].record(stream)
+        if record is not None:
+            record.append(marks)
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    rec = []
+    clk = ClockSampler(local)
+    with clk:
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(rec)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    for m in rec:
+        for i, k in enumerate(parts):
+            parts[k].append(m[i].elapsed_time(m[i + 1]))
+    part_ms = {k: statistics.median(v) for k, v in parts.items()}
+    # algorithmic bytes per phase (reads of keys / codes / scores, writes of codes / scores)
+    key_b, code_b = nq * S * d * 8, nq * S * 32
+    nb = len(budgets)
+    n_pages = (S + 15) // 16
+    alg = {"build": key_b + code_b, "select": nb * (code_b + 2 * nq * S * 4),
+           "quest": key_b + (1 + nb) * 2 * nq * n_pages * d * 8, "recall": key_b + nq * S * 8 * (1 + nb)}
+    dom = max(part_ms, key=part_ms.get)
+    peak, peak_kind = load_peaks()
+    achieved = alg[dom] / (part_ms[dom] * 1e-3) / 1e9
+    # e2e: the public run_sweep on host instances
+    sweep = _harness_sweep(H)
+    n_e2e = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        rows = H.run_sweep(insts, sweep)
+    torch.cuda.synchronize()
+    e2e_us = (time.perf_counter() - t0) * 1e6 / (n_e2e * nq)
+    hits = {c.budget: c.needle_fraction for c in H.needle_report(rows) if c.policy == "adamas-2bit-l1"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        v, sample = harness_cpu_reference(4)
+        cpu = {"value": v, "unit": HARNESS_UNIT, "cores": 1, "kind": "reference", "sample": sample}
+    launches = 1 + 3 * nb + 1 + 3 * nb + 1 + nb
+    line = {
+        "metric": HARNESS_METRIC, "value": ms * 1000.0 / nq, "unit": HARNESS_UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"acceptance needle sweep (acceptance.cpp:290-325 shape): {nq} planted-needle "
+                               f"queries per step, S={S}, d={d}, budgets {list(budgets)}, adamas-2bit-l1 + "
+                               f"window-sink4 + quest-p16, recall reference; numpy-generated instances",
+                   "l2": f"no flush: {key_b / 2**20:.0f} MiB of keys per step > 126 MB L2",
+                   "phase_ms": part_ms, "adamas_needle_fraction": hits},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": {"build": "hsel_encode_kernel", "select": "hsel_score+topk",
+                                                 "quest": "hsel_page_*", "recall": "hsel_dot+topk"}[dom],
+                     "bytes_per_launch": alg[dom], "phase": dom, "peak_source": peak_kind},
+        "e2e": {"value": e2e_us, "unit": HARNESS_UNIT,
+                "h2d_bytes_per_step": key_b + nq * d * 8, "d2h_bytes_per_step": nq * nb * 8 * (2 * 64 + 64)},
+        "gpu_launches": args.steps * launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+
+
+def run_harness_reference(args):
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    v, sample = harness_cpu_reference(max(2, min(args.steps, 8)))
+    print(json.dumps({
+        "impl": "reference", "metric": HARNESS_METRIC, "value": v, "unit": HARNESS_UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v / 1000.0, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "acceptance needle sweep (reference run_sweep, per query)"},
+        "cpu_baseline": {"value": v, "unit": HARNESS_UNIT, "cores": 1, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": HARNESS_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
 def main():
     args = parse()
+    if args.config == "harness_needle":
+        return run_harness_reference(args) if args.impl == "reference" else run_harness(args)
     if args.impl == "reference":
         run_reference(args)
     else:

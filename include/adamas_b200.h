@@ -244,9 +244,21 @@ int adamas_hsel_select(adamas_hsel* sel, const double* queries, int64_t n_rows, 
 int adamas_dot_topk(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst, int64_t n_inst,
                     int64_t seq_len, int head_dim, int64_t k, int64_t* idx, double* scores, void* stream);
 
-/* The quest baseline: PageSummaries (baselines.cpp:34-54) + page_select
- * (baselines.cpp:71-91). counts[r] = indices written for row r (the last page
- * may be partial). budget must be a multiple of page_size unless >= seq_len. */
+/* top_k_by_score (baselines.cpp:21-32) over given fp64 scores [n_rows][n]
+ * (e.g. the scores adamas_dot_topk returned, reused for several budgets). */
+int adamas_topk_f64(const double* scores, int64_t n_rows, int64_t n, int64_t k, int64_t* idx, void* stream);
+
+/* The quest baseline. PageSummaries (baselines.cpp:34-54) of n_inst key
+ * matrices, built once (prepare_state, sweep.cpp:68-72), then page_select
+ * (baselines.cpp:71-91) per budget: counts[r] = indices written for row r (the
+ * last page may be partial); budget must be a multiple of page_size unless
+ * >= seq_len. adamas_page_select is the one-shot form (synchronises). */
+typedef struct adamas_pages adamas_pages;
+int adamas_pages_create(adamas_pages** out, int64_t page_size, int head_dim);
+int adamas_pages_destroy(adamas_pages* pages);
+int adamas_pages_build(adamas_pages* pages, const double* keys, int64_t n_inst, int64_t seq_len, void* stream);
+int adamas_pages_select(adamas_pages* pages, const double* queries, int64_t n_rows, int64_t rows_per_inst,
+                        int64_t budget, int64_t* idx, int64_t* counts, void* stream);
 int adamas_page_select(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst,
                        int64_t n_inst, int64_t seq_len, int head_dim, int64_t page_size, int64_t budget, int64_t* idx,
                        int64_t* counts, void* stream);

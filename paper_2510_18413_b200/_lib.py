@@ -27,7 +27,8 @@ EXPORTED = [
     "adamas_seq_select_attend", "adamas_lse_merge", "adamas_cache_save_adkv", "adamas_cache_load_adkv",
     "adamas_score_metric", "adamas_hsel_create", "adamas_hsel_destroy", "adamas_hsel_build",
     "adamas_hsel_codes_ref", "adamas_hsel_select", "adamas_dot_topk", "adamas_page_select",
-    "adamas_attention_f64",
+    "adamas_attention_f64", "adamas_topk_f64", "adamas_pages_create", "adamas_pages_destroy",
+    "adamas_pages_build", "adamas_pages_select",
 ]
 
 
@@ -83,6 +84,11 @@ def load() -> C.CDLL:
     L.adamas_hsel_codes_ref.argtypes = [vp, i64, i64, vp, vp]
     L.adamas_hsel_select.argtypes = [vp, vp, i64, i64, i32, i64, vp, vp]
     L.adamas_dot_topk.argtypes = [vp, vp, i64, i64, i64, i64, i32, i64, vp, vp, vp]
+    L.adamas_pages_create.argtypes = [C.POINTER(vp), i64, i32]
+    L.adamas_pages_destroy.argtypes = [vp]
+    L.adamas_pages_build.argtypes = [vp, vp, i64, i64, vp]
+    L.adamas_pages_select.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
+    L.adamas_topk_f64.argtypes = [vp, i64, i64, i64, vp, vp]
     L.adamas_page_select.argtypes = [vp, vp, i64, i64, i64, i64, i32, i64, i64, vp, vp, vp]
     L.adamas_attention_f64.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp, vp]
     for name in EXPORTED:

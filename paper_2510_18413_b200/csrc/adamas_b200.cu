@@ -378,6 +378,15 @@ struct adamas_hsel {
   int* status = nullptr;       // device status word (kHselZero | kHselNonFinite)
 };
 
+// PageSummaries (baselines.cpp:34-54) of n_inst key matrices, device resident.
+struct adamas_pages {
+  int64_t page_size = 0, n_inst = 0, seq_len = 0;
+  int head_dim = 0;
+  double* mins = nullptr;  // [n_inst][pages][head_dim]; maxs follows in the same allocation
+  double* maxs = nullptr;
+  size_t cap = 0;
+};
+
 namespace {
 
 int grow_bytes(void** p, size_t* have, size_t need) {
@@ -402,7 +411,12 @@ int hsel_encode(int D, int bits, int hadamard, const double* x, int64_t n_vec, v
   const int grid = (int)std::min<int64_t>((n_vec + kHselWarps - 1) / kHselWarps, (int64_t)sm_count() * 16);
   uint32_t* pl = bits == 3 ? nullptr : static_cast<uint32_t*>(codes);
   uint8_t* by = bits == 3 ? static_cast<uint8_t*>(codes) : nullptr;
-#define HSEL_ENC(E_) hsel_encode_kernel<E_><<<grid, kHselWarps * 32, 0, s>>>(x, n_vec, D, bits, hadamard, pl, by, status)
+#define HSEL_ENC(E_)                                                                                      \
+  do {                                                                                                     \
+    if (bits == 1) hsel_encode_kernel<E_, 1><<<grid, kHselWarps * 32, 0, s>>>(x, n_vec, D, hadamard, pl, by, status); \
+    else if (bits == 2) hsel_encode_kernel<E_, 2><<<grid, kHselWarps * 32, 0, s>>>(x, n_vec, D, hadamard, pl, by, status); \
+    else hsel_encode_kernel<E_, 3><<<grid, kHselWarps * 32, 0, s>>>(x, n_vec, D, hadamard, pl, by, status); \
+  } while (0)
   switch (D >= 32 ? D / 32 : 1) {
     case 1: HSEL_ENC(1); break;
     case 2: HSEL_ENC(2); break;
@@ -426,6 +440,41 @@ int hsel_status_check(int* status, cudaStream_t s) {
   ADAMAS_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
   if (h & kHselNonFinite) return fail(ADAMAS_ERR_CONFIG, "non-finite input to compute_thresholds");
   return fail(ADAMAS_ERR_CONFIG, "degenerate scale: input vector is all zeros");
+}
+
+// Scratch of the harness entry points: stream-ordered allocations from a
+// library-owned pool that keeps freed memory (the default pool returns it to
+// the driver at every synchronisation, and re-mapping 100 MB buffers costs
+// milliseconds per call).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    if (cudaError_t e = cudaMemPoolCreate(&pool, &props)) return e;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = pool;
+  }
+  return cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 8), pools[dev], s);
+}
+
+// Grow a pool-backed buffer (freed stream-ordered into the retained pool, so
+// handles can be created and destroyed per sweep without driver unmaps).
+int pool_grow(void** p, size_t* have, size_t need, cudaStream_t s) {
+  if (*have >= need) return ADAMAS_OK;
+  if (*p) cudaFreeAsync(*p, s);
+  *p = nullptr;
+  *have = 0;
+  ADAMAS_CUDA(scratch_alloc(p, need, s));
+  *have = need;
+  return ADAMAS_OK;
 }
 
 int check_rows(int64_t n_rows, int64_t rows_per_inst, int64_t n_inst) {
@@ -917,7 +966,8 @@ int adamas_hsel_create(adamas_hsel** out, int head_dim, int bits, int with_hadam
   h->head_dim = head_dim;
   h->bits = bits;
   h->hadamard = with_hadamard ? 1 : 0;
-  if (cudaMalloc(&h->status, sizeof(int)) != cudaSuccess || cudaMemset(h->status, 0, sizeof(int)) != cudaSuccess) {
+  if (scratch_alloc(reinterpret_cast<void**>(&h->status), sizeof(int), 0) != cudaSuccess ||
+      cudaMemsetAsync(h->status, 0, sizeof(int), 0) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
     delete h;
     return fail(ADAMAS_ERR_RUNTIME, "hsel_create: cudaMalloc failed");
   }
@@ -927,11 +977,11 @@ int adamas_hsel_create(adamas_hsel** out, int head_dim, int bits, int with_hadam
 
 int adamas_hsel_destroy(adamas_hsel* h) {
   if (!h) return ADAMAS_OK;
-  cudaFree(h->planes);
-  cudaFree(h->bytes);
-  cudaFree(h->qcodes);
-  cudaFree(h->scores);
-  cudaFree(h->status);
+  // pool-backed buffers go back to the retained pool (no driver unmap) once
+  // every stream's queued work on them is done
+  cudaDeviceSynchronize();
+  for (void* b : {(void*)h->planes, (void*)h->bytes, h->qcodes, (void*)h->scores, (void*)h->status})
+    if (b) cudaFreeAsync(b, 0);
   delete h;
   return ADAMAS_OK;
 }
@@ -944,7 +994,7 @@ int adamas_hsel_build(adamas_hsel* h, const double* keys, int64_t n_inst, int64_
   const int64_t n_vec = n_inst * seq_len;
   const size_t need = std::max<size_t>(1, (size_t)n_vec * hsel_code_bytes(h->head_dim, h->bits));
   void** buf = h->bits == 3 ? reinterpret_cast<void**>(&h->bytes) : reinterpret_cast<void**>(&h->planes);
-  if (int rc = grow_bytes(buf, &h->code_cap, need)) return rc;
+  if (int rc = pool_grow(buf, &h->code_cap, need, s)) return rc;
   h->n_inst = n_inst;
   h->seq_len = seq_len;
   if (int rc = hsel_encode(h->head_dim, h->bits, h->hadamard, keys, n_vec, *buf, h->status, s)) return rc;
@@ -976,7 +1026,7 @@ int adamas_hsel_select(adamas_hsel* h, const double* queries, int64_t n_rows, in
   if (!queries || (budget > 0 && !idx)) return fail(ADAMAS_ERR_CONFIG, "hsel_select: null pointer");
   cudaStream_t s = as_stream(stream);
   const int D = h->head_dim;
-  if (int rc = grow_bytes(&h->qcodes, &h->q_cap, (size_t)n_rows * hsel_code_bytes(D, h->bits))) return rc;
+  if (int rc = pool_grow(&h->qcodes, &h->q_cap, (size_t)n_rows * hsel_code_bytes(D, h->bits), s)) return rc;
   if (int rc = hsel_encode(D, h->bits, h->hadamard, queries, n_rows, h->qcodes, h->status, s)) return rc;
   if (int rc = hsel_status_check(h->status, s)) return rc;
   const int64_t S = h->seq_len;
@@ -986,7 +1036,7 @@ int adamas_hsel_select(adamas_hsel* h, const double* queries, int64_t n_rows, in
     return ADAMAS_OK;
   }
   void* sc = h->scores;
-  if (int rc = grow_bytes(&sc, &h->scores_cap, (size_t)n_rows * S * sizeof(uint32_t))) return rc;
+  if (int rc = pool_grow(&sc, &h->scores_cap, (size_t)n_rows * S * sizeof(uint32_t), s)) return rc;
   h->scores = static_cast<uint32_t*>(sc);
   const dim3 grid((unsigned)((S + kHselScoreThreads - 1) / kHselScoreThreads), (unsigned)n_rows);
   const uint32_t* qp = h->bits == 3 ? nullptr : static_cast<const uint32_t*>(h->qcodes);
@@ -1010,54 +1060,103 @@ int adamas_dot_topk(const double* queries, const double* keys, int64_t n_rows, i
   if (n_rows == 0) return ADAMAS_OK;
   cudaStream_t s = as_stream(stream);
   double* sc = scores;
-  if (!sc) ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), std::max<size_t>(8, (size_t)n_rows * seq_len * 8), s));
+  if (!sc) ADAMAS_CUDA(scratch_alloc(reinterpret_cast<void**>(&sc), (size_t)n_rows * seq_len * 8, s));
   int rc = dot_scores(queries, keys, n_rows, rows_per_inst, seq_len, head_dim, sc, s);
   if (!rc && k > 0) rc = topk_launch(1, sc, n_rows, seq_len, k, idx, s);
   if (!scores) cudaFreeAsync(sc, s);
   return rc;
 }
 
+int adamas_topk_f64(const double* scores, int64_t n_rows, int64_t n, int64_t k, int64_t* idx, void* stream) {
+  if (n_rows < 0 || n < 0 || k < 0) return fail(ADAMAS_ERR_CONFIG, "topk_f64: negative size");
+  if (n_rows == 0 || k == 0) return ADAMAS_OK;
+  if (!scores || !idx) return fail(ADAMAS_ERR_CONFIG, "topk_f64: null pointer");
+  return topk_launch(1, scores, n_rows, n, k, idx, as_stream(stream));
+}
+
+int adamas_pages_create(adamas_pages** out, int64_t page_size, int head_dim) {
+  if (!out) return fail(ADAMAS_ERR_CONFIG, "pages_create: null out");
+  *out = nullptr;
+  if (page_size < 1) return fail(ADAMAS_ERR_CONFIG, "PageSummaries: page_size must be positive");
+  if (head_dim < 1 || head_dim > kHselMaxDim) return fail(ADAMAS_ERR_CONFIG, "PageSummaries: head_dim out of range");
+  auto* p = new adamas_pages();
+  p->page_size = page_size;
+  p->head_dim = head_dim;
+  *out = p;
+  return ADAMAS_OK;
+}
+
+int adamas_pages_destroy(adamas_pages* p) {
+  if (!p) return ADAMAS_OK;
+  cudaDeviceSynchronize();
+  if (p->mins) cudaFreeAsync(p->mins, 0);
+  delete p;
+  return ADAMAS_OK;
+}
+
+int adamas_pages_build(adamas_pages* p, const double* keys, int64_t n_inst, int64_t seq_len, void* stream) {
+  if (!p) return fail(ADAMAS_ERR_CONFIG, "null pages handle");
+  if (n_inst < 0 || seq_len < 0) return fail(ADAMAS_ERR_CONFIG, "pages_build: negative size");
+  const int64_t P = (seq_len + p->page_size - 1) / p->page_size;
+  const size_t half = (size_t)n_inst * P * p->head_dim;
+  void* buf = p->mins;
+  if (int rc = pool_grow(&buf, &p->cap, std::max<size_t>(16, 2 * half * sizeof(double)), as_stream(stream))) return rc;
+  p->mins = static_cast<double*>(buf);
+  p->maxs = p->mins + half;
+  p->n_inst = n_inst;
+  p->seq_len = seq_len;
+  if (half == 0) return ADAMAS_OK;
+  if (!keys) return fail(ADAMAS_ERR_CONFIG, "pages_build: null keys");
+  const int g = (int)std::min<int64_t>(((int64_t)half + 255) / 256, (int64_t)sm_count() * 16);
+  hsel_page_summary_kernel<<<g, 256, 0, as_stream(stream)>>>(keys, n_inst, seq_len, p->head_dim, p->page_size,
+                                                              p->mins, p->maxs);
+  return launch_check("hsel_page_summary_kernel");
+}
+
+int adamas_pages_select(adamas_pages* p, const double* queries, int64_t n_rows, int64_t rows_per_inst, int64_t budget,
+                        int64_t* idx, int64_t* counts, void* stream) {
+  if (!p) return fail(ADAMAS_ERR_CONFIG, "null pages handle");
+  if (budget < 0) return fail(ADAMAS_ERR_CONFIG, "page_select: negative budget");
+  if (int rc = check_rows(n_rows, rows_per_inst, p->n_inst)) return rc;
+  if (n_rows == 0 || budget == 0) return ADAMAS_OK;
+  if (n_rows > 65535) return fail(ADAMAS_ERR_CONFIG, "page_select: at most 65535 query rows per call");
+  if (!queries || !idx || !counts) return fail(ADAMAS_ERR_CONFIG, "page_select: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t S = p->seq_len, ps_ = p->page_size;
+  if (budget >= S) {  // baselines.cpp:74-78: everything
+    hsel_topk_kernel<0><<<(unsigned)n_rows, kHselTopkThreads, 0, s>>>(nullptr, S, budget, idx);
+    if (int rc = launch_check("hsel_topk_kernel")) return rc;
+    hsel_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(counts, n_rows, S);
+    return launch_check("hsel_fill_kernel");
+  }
+  if (budget % ps_ != 0) return fail(ADAMAS_ERR_CONFIG, "page_select: budget must be a multiple of the page size");
+  const int64_t P = (S + ps_ - 1) / ps_, kp = budget / ps_;
+  double* sc = nullptr;
+  int64_t* pages = nullptr;
+  ADAMAS_CUDA(scratch_alloc(reinterpret_cast<void**>(&sc), (size_t)n_rows * P * 8, s));
+  ADAMAS_CUDA(scratch_alloc(reinterpret_cast<void**>(&pages), (size_t)n_rows * kp * 8, s));
+  const dim3 grid((unsigned)((P + kHselPageTile - 1) / kHselPageTile), (unsigned)n_rows);
+  hsel_page_score_kernel<<<grid, kHselPageTile, 0, s>>>(queries, p->mins, p->maxs, rows_per_inst, P, p->head_dim, sc);
+  int rc = launch_check("hsel_page_score_kernel");
+  if (!rc) rc = topk_launch(1, sc, n_rows, P, kp, pages, s);
+  if (!rc) {
+    hsel_page_expand_kernel<<<(unsigned)n_rows, 256, 0, s>>>(pages, kp, S, ps_, budget, idx, counts);
+    rc = launch_check("hsel_page_expand_kernel");
+  }
+  cudaFreeAsync(sc, s);
+  cudaFreeAsync(pages, s);
+  return rc;
+}
+
 int adamas_page_select(const double* queries, const double* keys, int64_t n_rows, int64_t rows_per_inst,
                        int64_t n_inst, int64_t seq_len, int head_dim, int64_t page_size, int64_t budget, int64_t* idx,
                        int64_t* counts, void* stream) {
-  if (page_size < 1) return fail(ADAMAS_ERR_CONFIG, "PageSummaries: page_size must be positive");
-  if (head_dim < 1 || head_dim > kHselMaxDim) return fail(ADAMAS_ERR_CONFIG, "page_select: head_dim out of range");
-  if (budget < 0 || seq_len < 0) return fail(ADAMAS_ERR_CONFIG, "page_select: negative size");
-  if (int rc = check_rows(n_rows, rows_per_inst, n_inst)) return rc;
-  if (n_rows == 0 || budget == 0) return ADAMAS_OK;
-  cudaStream_t s = as_stream(stream);
-  if (n_rows > 0x7fffffff) return fail(ADAMAS_ERR_CONFIG, "page_select: too many rows");
-  if (budget >= seq_len) {  // baselines.cpp:74-78: everything
-    hsel_topk_kernel<0><<<(unsigned)n_rows, kHselTopkThreads, 0, s>>>(nullptr, seq_len, budget, idx);
-    if (int rc = launch_check("hsel_topk_kernel")) return rc;
-    hsel_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(counts, n_rows, seq_len);
-    return launch_check("hsel_fill_kernel");
-  }
-  if (budget % page_size != 0) return fail(ADAMAS_ERR_CONFIG, "page_select: budget must be a multiple of the page size");
-  const int64_t P = (seq_len + page_size - 1) / page_size, kp = budget / page_size;
-  double *mins = nullptr, *maxs = nullptr, *ps = nullptr;
-  int64_t* pages = nullptr;
-  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mins), (size_t)n_inst * P * head_dim * 8, s));
-  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&maxs), (size_t)n_inst * P * head_dim * 8, s));
-  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ps), (size_t)n_rows * P * 8, s));
-  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pages), (size_t)n_rows * kp * 8, s));
-  const int g1 = (int)std::min<int64_t>((n_inst * P * head_dim + 255) / 256, (int64_t)sm_count() * 16);
-  hsel_page_summary_kernel<<<std::max(g1, 1), 256, 0, s>>>(keys, n_inst, seq_len, head_dim, page_size, mins, maxs);
-  int rc = launch_check("hsel_page_summary_kernel");
-  if (!rc) {
-    const int g2 = (int)std::min<int64_t>((n_rows * P + 255) / 256, (int64_t)sm_count() * 16);
-    hsel_page_score_kernel<<<std::max(g2, 1), 256, 0, s>>>(queries, mins, maxs, n_rows, rows_per_inst, P, head_dim, ps);
-    rc = launch_check("hsel_page_score_kernel");
-  }
-  if (!rc) rc = topk_launch(1, ps, n_rows, P, kp, pages, s);
-  if (!rc) {
-    hsel_page_expand_kernel<<<(unsigned)n_rows, 256, 0, s>>>(pages, kp, seq_len, page_size, budget, idx, counts);
-    rc = launch_check("hsel_page_expand_kernel");
-  }
-  cudaFreeAsync(mins, s);
-  cudaFreeAsync(maxs, s);
-  cudaFreeAsync(ps, s);
-  cudaFreeAsync(pages, s);
+  adamas_pages* p = nullptr;
+  if (int rc = adamas_pages_create(&p, page_size, head_dim)) return rc;
+  int rc = adamas_pages_build(p, keys, n_inst, seq_len, stream);
+  if (!rc) rc = adamas_pages_select(p, queries, n_rows, rows_per_inst, budget, idx, counts, stream);
+  if (!rc) rc = cudaStreamSynchronize(as_stream(stream)) == cudaSuccess ? ADAMAS_OK : fail(ADAMAS_ERR_RUNTIME, "page_select: sync");
+  adamas_pages_destroy(p);
   return rc;
 }
 
@@ -1072,7 +1171,7 @@ int adamas_attention_f64(const double* queries, const double* keys, const double
   cudaStream_t s = as_stream(stream);
   const int64_t n_max = idx ? idx_stride : seq_len;
   double* lg = nullptr;
-  ADAMAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lg), (size_t)n_rows * n_max * 8, s));
+  ADAMAS_CUDA(scratch_alloc(reinterpret_cast<void**>(&lg), (size_t)n_rows * n_max * 8, s));
   hsel_attention_kernel<<<(unsigned)n_rows, kHselAttnThreads, 0, s>>>(queries, keys, values, seq_len, head_dim,
                                                                        rows_per_inst, idx, idx_stride, counts, lg,
                                                                        n_max, out);

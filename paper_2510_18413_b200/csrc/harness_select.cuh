@@ -72,12 +72,13 @@ __device__ __forceinline__ void hsel_fwht(double (&x)[E], int D) {
 
 // One warp per vector. planes: [n_vec][2][W] u32 (low code bit, low ^ high
 // bit) for bits 1 and 2; bytes: [n_vec][D] (the reference's CodeVector) for 3.
-template <int E>
+template <int E, int BITS>
 __global__ void __launch_bounds__(kHselWarps * 32)
-hsel_encode_kernel(const double* __restrict__ x, int64_t n_vec, int D, int bits, int hadamard,
+hsel_encode_kernel(const double* __restrict__ x, int64_t n_vec, int D, int hadamard,
                    uint32_t* __restrict__ planes, uint8_t* __restrict__ bytes, int* __restrict__ status) {
   __shared__ double sq[kHselWarps][32 * E];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int bits = BITS;
   const bool active = lane * E < D;
   const int W = hsel_words(D);
   for (int64_t v = (int64_t)blockIdx.x * kHselWarps + warp; v < n_vec; v += (int64_t)gridDim.x * kHselWarps) {
@@ -86,20 +87,49 @@ hsel_encode_kernel(const double* __restrict__ x, int64_t n_vec, int D, int bits,
 #pragma unroll
     for (int e = 0; e < E; ++e) r[e] = active ? src[e] : 0.0;
     if (hadamard) hsel_fwht<E>(r, D);
-    // compute_thresholds: sum of squares in index order 0..D-1 (quantizer.cpp:43-44)
-    if (active) {
+    // compute_thresholds: sum of squares in index order 0..D-1 (quantizer.cpp:43-44).
+    // Fast path: a shuffle-tree sum of the same exact products. Two summation
+    // orders of n <= 1024 non-negative terms agree to 2 (n - 1) u < 2.3e-13
+    // relative, so sigma and every threshold k * sigma agree to < 2e-13; the
+    // codes can only differ for an element within that distance of a nonzero
+    // threshold (0 does not depend on sigma). If any element is within 1e-12
+    // relative of one, or the sum is near the ends of the fp64 range, the warp
+    // takes the exact sequential sum instead.
+    double sqv[E];
+    double s4 = 0.0;
 #pragma unroll
-      for (int e = 0; e < E; ++e) sq[warp][lane * E + e] = __dmul_rn(r[e], r[e]);
+    for (int e = 0; e < E; ++e) {
+      sqv[e] = active ? __dmul_rn(r[e], r[e]) : 0.0;
+      s4 = __dadd_rn(s4, sqv[e]);
     }
-    __syncwarp();
-    double sigma = 0.0;
-    if (lane == 0) {
-      double acc = 0.0;
-      for (int j = 0; j < D; ++j) acc = __dadd_rn(acc, sq[warp][j]);
-      sigma = __dsqrt_rn(__ddiv_rn(acc, (double)D));
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) s4 = __dadd_rn(s4, __shfl_xor_sync(kFull, s4, m));
+    double sigma = __dsqrt_rn(__ddiv_rn(s4, (double)D));
+    bool near = !(s4 > 1e-290 && s4 < 1e300);
+    if (bits >= 2) {
+      const double t28 = __dmul_rn(kQ28, sigma);
+      const double t18 = __dmul_rn(kQ18, sigma), t38 = __dmul_rn(kQ38, sigma);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double a = fabs(r[e]);
+        near |= fabs(a - t28) <= 1e-12 * t28;
+        if (bits == 3) near |= fabs(a - t18) <= 1e-12 * t18 || fabs(a - t38) <= 1e-12 * t38;
+      }
     }
-    sigma = __shfl_sync(kFull, sigma, 0);
-    __syncwarp();  // sq is rewritten for the next vector
+    if (__any_sync(kFull, near)) {
+      if (active) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) sq[warp][lane * E + e] = sqv[e];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        double acc = 0.0;
+        for (int j = 0; j < D; ++j) acc = __dadd_rn(acc, sq[warp][j]);
+        sigma = __dsqrt_rn(__ddiv_rn(acc, (double)D));
+      }
+      sigma = __shfl_sync(kFull, sigma, 0);
+      __syncwarp();  // sq is rewritten for the next vector
+    }
     const int bad = !isfinite(sigma) ? kHselNonFinite : (sigma == 0.0 ? kHselZero : 0);
     if (bad && lane == 0) atomicOr(status, bad);
     // thresholds (quantizer.cpp:52-62): -k s is (-k) s, exactly -(k s)
@@ -434,22 +464,37 @@ __global__ void hsel_page_summary_kernel(const double* __restrict__ keys, int64_
 }
 
 // page_scores (baselines.cpp:57-69): s += std::max(q_j mn_j, q_j mx_j), j ascending.
-__global__ void hsel_page_score_kernel(const double* __restrict__ q, const double* __restrict__ mins,
-                                       const double* __restrict__ maxs, int64_t n_rows, int64_t rows_per_inst,
-                                       int64_t P, int D, double* __restrict__ scores) {
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_rows * P;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = g / P, p = g % P, inst = row / rows_per_inst;
-    const double* qq = q + row * D;
-    const double* mn = mins + (inst * P + p) * D;
-    const double* mx = maxs + (inst * P + p) * D;
-    double s = 0.0;
-    for (int j = 0; j < D; ++j) {
-      const double a = __dmul_rn(qq[j], mn[j]), b = __dmul_rn(qq[j], mx[j]);
-      s = __dadd_rn(s, a < b ? b : a);
+// CTA = 128 pages of one query row; page summaries staged 16 channels at a time.
+constexpr int kHselPageTile = 128;
+
+__global__ void __launch_bounds__(kHselPageTile)
+hsel_page_score_kernel(const double* __restrict__ q, const double* __restrict__ mins, const double* __restrict__ maxs,
+                       int64_t rows_per_inst, int64_t P, int D, double* __restrict__ scores) {
+  __shared__ double qs[kHselMaxDim];
+  __shared__ double tmn[kHselPageTile][17], tmx[kHselPageTile][17];
+  const int64_t row = blockIdx.y, inst = row / rows_per_inst;
+  const int64_t p0 = (int64_t)blockIdx.x * kHselPageTile;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) qs[j] = q[row * D + j];
+  const double* mn = mins + inst * P * D;
+  const double* mx = maxs + inst * P * D;
+  double sc = 0.0;
+  for (int j0 = 0; j0 < D; j0 += 16) {
+    const int jw = D - j0 < 16 ? D - j0 : 16;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHselPageTile * 16; i += kHselPageTile) {
+      const int r = i >> 4, c = i & 15;
+      const int64_t pr = p0 + r;
+      const bool ok = pr < P && c < jw;
+      tmn[r][c] = ok ? mn[pr * D + j0 + c] : 0.0;
+      tmx[r][c] = ok ? mx[pr * D + j0 + c] : 0.0;
     }
-    scores[g] = s;
+    __syncthreads();
+    for (int c = 0; c < jw; ++c) {
+      const double a = __dmul_rn(qs[j0 + c], tmn[threadIdx.x][c]), b = __dmul_rn(qs[j0 + c], tmx[threadIdx.x][c]);
+      sc = __dadd_rn(sc, a < b ? b : a);
+    }
   }
+  if (p0 + threadIdx.x < P) scores[row * P + p0 + threadIdx.x] = sc;
 }
 
 // page_select (baselines.cpp:71-91): the selected pages (ascending) expanded to

@@ -184,6 +184,15 @@ def _dev(a, device) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(device)
 
 
+def _dev_stack(arrays, device) -> torch.Tensor:
+    """Stack host fp64 matrices straight into one device tensor (one H2D copy
+    per matrix, no host-side concatenation)."""
+    out = torch.empty((len(arrays), *arrays[0].shape), dtype=torch.float64, device=device)
+    for i, a in enumerate(arrays):
+        out[i].copy_(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)))
+    return out
+
+
 class HarnessSelector:
     """One adamas policy's code store: build_cache over n_inst key matrices,
     then select for any number of queries (sweep.cpp:38-50, :87-98)."""
@@ -244,6 +253,47 @@ def dot_topk(queries, keys, k: int, rows_per_inst: int = 1, want_scores: bool = 
     check(L.adamas_dot_topk(_ptr(queries), _ptr(keys), n_rows, rows_per_inst, n_inst, S, d, k, _ptr(idx), _ptr(sc),
                             _stream()))
     return (idx, sc) if want_scores else idx
+
+
+def topk_scores(scores, k: int):
+    """top_k_by_score over precomputed fp64 scores [n_rows][n]."""
+    L = load()
+    idx = torch.empty((scores.shape[0], k), dtype=torch.int64, device=scores.device)
+    check(L.adamas_topk_f64(_ptr(scores), scores.shape[0], scores.shape[1], k, _ptr(idx), _stream()))
+    return idx
+
+
+class PageSelector:
+    """The quest baseline's state: PageSummaries of n_inst key matrices
+    (baselines.cpp:34-54), built once, then page_select per budget (:71-91)."""
+
+    def __init__(self, page_size: int, head_dim: int):
+        self.h = None
+        self.L = load()
+        h = C.c_void_p()
+        check(self.L.adamas_pages_create(C.byref(h), page_size, head_dim))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.L.adamas_pages_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def build(self, keys: torch.Tensor) -> None:
+        keys = keys.contiguous()
+        check(self.L.adamas_pages_build(self.h, _ptr(keys), keys.shape[0], keys.shape[1], _stream()))
+
+    def select(self, queries: torch.Tensor, budget: int, rows_per_inst: int = 1):
+        """(idx [n_rows][budget], counts [n_rows])."""
+        queries = queries.contiguous()
+        n = queries.shape[0]
+        idx = torch.empty((n, budget), dtype=torch.int64, device=queries.device)
+        counts = torch.zeros(n, dtype=torch.int64, device=queries.device)
+        check(self.L.adamas_pages_select(self.h, _ptr(queries), n, rows_per_inst, budget, _ptr(idx), _ptr(counts),
+                                         _stream()))
+        return idx, counts
 
 
 def page_select(queries, keys, page_size: int, budget: int, rows_per_inst: int = 1):
@@ -319,19 +369,24 @@ def run_sweep(instances: Sequence[Instance], sweep: SweepConfig, device: str = "
     rpi = n_q // n_inst
     if n_q % n_inst or any(of[r] != r // rpi for r in range(n_q)):
         return _run_sweep_grouped(instances, sweep, device)
-    K = _dev(np.stack([u.keys for u in uniq]), device)
-    V = _dev(np.stack([u.values for u in uniq]), device)
+    K = _dev_stack([u.keys for u in uniq], device)
+    V = _dev_stack([u.values for u in uniq], device) if sweep.measure_output_error else None
     Q = _dev(np.stack([i.query for i in instances]), device)
     budgets = list(sweep.budgets)
-    oracle = {b: dot_topk(Q, K, b, rpi).cpu().numpy() for b in budgets}
+    _, dots = dot_topk(Q, K, 0, rpi, want_scores=True)  # dot scores once, top-k per budget
+    oracle = {b: topk_scores(dots, b).cpu().numpy() for b in budgets}
+    del dots
     exact = attention_f64(Q, K, V, rpi).cpu().numpy() if sweep.measure_output_error else None
     rows = []
     for pol in sweep.policies:
         label = pol.label()
         sel_state = None
-        if pol.kind == "adamas":
+        if pol.kind == "adamas":  # prepare_state (sweep.cpp:60-78): errors are not cell-qualified
             sel_state = HarnessSelector(d, pol.bits, pol.with_hadamard)
-            sel_state.build(K)  # prepare_state (sweep.cpp:60-78): errors are not cell-qualified
+            sel_state.build(K)
+        elif pol.kind == "quest":
+            sel_state = PageSelector(pol.page_size, d)
+            sel_state.build(K)
         try:
             for b in budgets:
                 try:
@@ -345,22 +400,30 @@ def run_sweep(instances: Sequence[Instance], sweep: SweepConfig, device: str = "
                     approx = attention_f64(Q, K, V, rpi, idx, counts).cpu().numpy()
                 idx_h = idx.cpu().numpy()
                 cnt_h = counts.cpu().numpy()
+                common = _common_counts(idx_h, oracle[b])
+                n_orc = min(b, S)
                 for qi, inst in enumerate(instances):
                     n = int(cnt_h[qi])
-                    sel = idx_h[qi, :n]
-                    orc = oracle[b][qi, :min(b, S)]
                     row = ResultRow(policy=label, budget=b, seed=inst.seed)
-                    row.recall = recall_against(sel, orc)
+                    # recall_against (sweep.cpp:113-118); n_orc > 0 always (b, S >= 1)
+                    row.recall = float(common[qi]) / float(n_orc)
                     row.selected_count = n
                     if approx is not None:
                         row.output_error = output_error(approx[qi], exact[qi])
                     if inst.needle_position is not None:
-                        row.needle_hit = bool(np.isin(inst.needle_position, sel))
+                        row.needle_hit = bool((idx_h[qi, :n] == inst.needle_position).any())
                     rows.append(row)
         finally:
             if sel_state is not None:
                 sel_state.close()
     return rows
+
+
+def _common_counts(sel: np.ndarray, orc: np.ndarray) -> np.ndarray:
+    """|sel_r ∩ orc_r| per row; rows hold distinct indices, -1 padded."""
+    m = np.concatenate([sel, orc], axis=1)
+    m.sort(axis=1)
+    return ((m[:, 1:] == m[:, :-1]) & (m[:, 1:] >= 0)).sum(axis=1)
 
 
 def _select(pol, selector, Q, K, b, rpi, S, oracle):
@@ -370,7 +433,7 @@ def _select(pol, selector, Q, K, b, rpi, S, oracle):
     if pol.kind == "oracle":
         return torch.as_tensor(oracle[b], device=Q.device), None
     if pol.kind == "quest":
-        return page_select(Q, K, pol.page_size, b, rpi)
+        return selector.select(Q, b, rpi)
     # window (baselines.cpp:8-19; sweep.cpp:100-104): index arithmetic only
     sink = min(pol.sink, b)
     recent = b - sink

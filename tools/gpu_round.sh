@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/pyt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 2 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for c in llama128k batched16 seqshard1m; do
+for c in llama128k batched16 seqshard1m harness_needle; do
   timeout 600 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/cfg_$c.json 2> gpurun_out/cfg_$c.err
 done
 timeout 300 python tools/prefill_bench.py > gpurun_out/prefill.json 2>&1
