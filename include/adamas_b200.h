@@ -198,6 +198,41 @@ int adamas_seq_select_attend(const adamas_cache* cache, const void* q, int n_q_h
  * out float32 [n_q][128]. */
 int adamas_lse_merge(const float* partials, int n_ranks, int n_q_heads, float* out, void* stream);
 
+/* ---------------------------------------------------------------- sequence sharding over peer memory
+ * The same three phases as adamas_seq_local_candidates / _select_attend /
+ * _lse_merge, with the two all-gathers replaced by stores into every rank's
+ * mailbox over NVLink: phase 1's fused kernel writes its candidate keys
+ * straight into all mailboxes and publishes an epoch (system-scope release);
+ * phase 2 acquires every rank's keys epoch, selects + attends, and writes its
+ * partial into all mailboxes; phase 3 acquires the partial epochs and merges.
+ * No NCCL call, no host synchronisation, graph-capturable. Mailboxes are
+ * cudaMalloc'd (CUDA IPC); ranks exchange the 64-byte handles once at setup
+ * (any transport: torch.distributed all_gather_object, MPI, a file) and call
+ * adamas_mailbox_connect. Ranks of one process (tests, one GPU) use
+ * adamas_mailbox_connect_local. A wait that exceeds ~4 s latches
+ * ADAMAS_STATUS_PEER_TIMEOUT (adamas_mailbox_status) instead of hanging. */
+#define ADAMAS_IPC_HANDLE_BYTES 64
+#define ADAMAS_STATUS_PEER_TIMEOUT 8
+typedef struct adamas_mailbox adamas_mailbox;
+int adamas_mailbox_create(adamas_mailbox** out, int rank, int world, int n_q_heads, int64_t budget);
+int adamas_mailbox_ipc_handle(const adamas_mailbox* mailbox, void* handle);
+int adamas_mailbox_connect(adamas_mailbox* mailbox, const void* handles /* world x 64 B, rank order */);
+int adamas_mailbox_connect_local(adamas_mailbox* const* mailboxes, int world);
+int adamas_mailbox_status(adamas_mailbox* mailbox, int* status);
+int adamas_mailbox_destroy(adamas_mailbox* mailbox);
+/* phase 1: append (tail rank) + local candidates, pushed to every rank; advances the epoch */
+int adamas_seq_p2p_local(adamas_cache* cache, adamas_mailbox* mailbox, const void* q, int n_q_heads, const void* k_new,
+                         const void* v_new, int append, int64_t base_index, void* stream);
+/* phase 2: wait for every rank's keys, global select, attend this rank's survivors, push the partial */
+int adamas_seq_p2p_select_attend(const adamas_cache* cache, adamas_mailbox* mailbox, const void* q, int n_q_heads,
+                                 int64_t total_len, int64_t rank_base, int32_t* global_idx, void* stream);
+/* phase 3: wait for every rank's partial, log-sum-exp merge -> out [n_q][128] f32 */
+int adamas_seq_p2p_merge(adamas_mailbox* mailbox, float* out, void* stream);
+/* phases 1-3 */
+int adamas_seq_step_p2p(adamas_cache* cache, adamas_mailbox* mailbox, const void* q, int n_q_heads, const void* k_new,
+                        const void* v_new, int append, int64_t base_index, int64_t total_len, float* out,
+                        int32_t* global_idx, void* stream);
+
 /* ---------------------------------------------------------------- f3: harness selection backend
  * The sweep harness's selection step on the GPU, in the
  * harness's own arithmetic: fp64 inputs, any power-of-two head_dim in

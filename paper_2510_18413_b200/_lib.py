@@ -28,7 +28,9 @@ EXPORTED = [
     "adamas_score_metric", "adamas_hsel_create", "adamas_hsel_destroy", "adamas_hsel_build",
     "adamas_hsel_codes_ref", "adamas_hsel_select", "adamas_dot_topk", "adamas_page_select",
     "adamas_attention_f64", "adamas_topk_f64", "adamas_pages_create", "adamas_pages_destroy",
-    "adamas_pages_build", "adamas_pages_select",
+    "adamas_pages_build", "adamas_pages_select", "adamas_mailbox_create", "adamas_mailbox_ipc_handle",
+    "adamas_mailbox_connect", "adamas_mailbox_connect_local", "adamas_mailbox_status", "adamas_mailbox_destroy",
+    "adamas_seq_p2p_local", "adamas_seq_p2p_select_attend", "adamas_seq_p2p_merge", "adamas_seq_step_p2p",
 ]
 
 
@@ -88,6 +90,16 @@ def load() -> C.CDLL:
     L.adamas_pages_destroy.argtypes = [vp]
     L.adamas_pages_build.argtypes = [vp, vp, i64, i64, vp]
     L.adamas_pages_select.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp]
+    L.adamas_mailbox_create.argtypes = [C.POINTER(vp), i32, i32, i32, i64]
+    L.adamas_mailbox_ipc_handle.argtypes = [vp, vp]
+    L.adamas_mailbox_connect.argtypes = [vp, vp]
+    L.adamas_mailbox_connect_local.argtypes = [C.POINTER(vp), i32]
+    L.adamas_mailbox_status.argtypes = [vp, C.POINTER(i32)]
+    L.adamas_mailbox_destroy.argtypes = [vp]
+    L.adamas_seq_p2p_local.argtypes = [vp, vp, vp, i32, vp, vp, i32, i64, vp]
+    L.adamas_seq_p2p_select_attend.argtypes = [vp, vp, vp, i32, i64, i64, vp, vp]
+    L.adamas_seq_p2p_merge.argtypes = [vp, vp, vp]
+    L.adamas_seq_step_p2p.argtypes = [vp, vp, vp, i32, vp, vp, i32, i64, i64, vp, vp, vp]
     L.adamas_topk_f64.argtypes = [vp, i64, i64, i64, vp, vp]
     L.adamas_page_select.argtypes = [vp, vp, i64, i64, i64, i64, i32, i64, i64, vp, vp, vp]
     L.adamas_attention_f64.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp, vp]

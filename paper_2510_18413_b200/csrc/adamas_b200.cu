@@ -229,7 +229,7 @@ int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaSt
 int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n_q, int dtype, const void* q,
                         const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
                         cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0,
-                        int qsplit = 0) {
+                        int qsplit = 0, const PeerPush* peers = nullptr) {
   if (qsplit == 0) {  // auto
     // Clusters above 4 CTAs do not reach a full wave of co-resident CTAs on
     // B200 (measured): take the smallest split of a kv-head's q-heads over
@@ -313,6 +313,7 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
           if (int rc = ensure_unit_scratch(caches[i], (size_t)n_kv * qsplit * P * G)) return rc;
       prm.cand = cand;
       prm.cand_base = cand_base;
+      prm.peers = peers ? *peers : PeerPush{};
       prm.q = q;
       prm.k_new = k_new;
       prm.v_new = v_new;
@@ -378,6 +379,23 @@ struct adamas_hsel {
   int* status = nullptr;       // device status word (kHselZero | kHselNonFinite)
 };
 
+// Peer-memory exchange of the sequence-sharded decode: one mailbox
+// per rank in its own HBM, mapped into every rank through CUDA IPC.
+//   keys      [world][n_q][budget] u32   slot r written by rank r (phase 1)
+//   partials  [world][n_q][132] f32      slot r written by rank r (phase 2)
+//   key_flag  [32] u32, part_flag [32] u32   epoch published by rank r
+//   arrive    [2] u32 (own launches' CTA arrival counters; padded lines)
+struct adamas_mailbox {
+  int rank = 0, world = 1, n_q = 0;
+  int64_t budget = 0;
+  size_t keys_off = 0, part_off = 0, kflag_off = 0, pflag_off = 0, arrive_off = 0, bytes = 0;
+  char* base = nullptr;                 // own mailbox (cudaMalloc: IPC-exportable)
+  char* peer[kMaxPeers] = {};           // every rank's mailbox as mapped here (peer[rank] = base)
+  bool ipc_opened[kMaxPeers] = {};
+  uint32_t epoch = 0;
+  int* status = nullptr;
+};
+
 // PageSummaries (baselines.cpp:34-54) of n_inst key matrices, device resident.
 struct adamas_pages {
   int64_t page_size = 0, n_inst = 0, seq_len = 0;
@@ -388,16 +406,6 @@ struct adamas_pages {
 };
 
 namespace {
-
-int grow_bytes(void** p, size_t* have, size_t need) {
-  if (*have >= need) return ADAMAS_OK;
-  if (*p) cudaFree(*p);
-  *p = nullptr;
-  *have = 0;
-  ADAMAS_CUDA(cudaMalloc(p, need));
-  *have = need;
-  return ADAMAS_OK;
-}
 
 bool pow2_dim(int d) { return d >= 2 && d <= kHselMaxDim && (d & (d - 1)) == 0; }
 
@@ -794,18 +802,18 @@ int adamas_seq_select_attend(const adamas_cache* c, const void* q, int n_q, cons
   if (c->dtype == ADAMAS_BF16)
     seq_select_attend_kernel<__nv_bfloat16><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
         (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, gathered,
-        n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx);
+        n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{}, nullptr, c->status);
   else
     seq_select_attend_kernel<float><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
         (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, gathered, n_ranks, n_q, budget,
-        k_eff, rank_base, c->seq_len, partial, global_idx);
+        k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{}, nullptr, c->status);
   return launch_check("seq_select_attend_kernel");
 }
 
 int adamas_lse_merge(const float* partials, int n_ranks, int n_q, float* out, void* stream) {
   if (n_ranks < 1 || n_q < 1) return fail(ADAMAS_ERR_CONFIG, "lse_merge: bad sizes");
   if (!partials || !out) return fail(ADAMAS_ERR_CONFIG, "lse_merge: null pointer");
-  lse_merge_kernel<<<n_q, 32, 0, as_stream(stream)>>>(partials, n_ranks, n_q, out);
+  lse_merge_kernel<<<n_q, 32, 0, as_stream(stream)>>>(partials, n_ranks, n_q, out, nullptr, 0, nullptr);
   return launch_check("lse_merge_kernel");
 }
 
@@ -1178,6 +1186,190 @@ int adamas_attention_f64(const double* queries, const double* keys, const double
   const int rc = launch_check("hsel_attention_kernel");
   cudaFreeAsync(lg, s);
   return rc;
+}
+
+// ---------------------------------------------------------------- peer-memory sequence sharding
+namespace {
+PeerPush key_push(const adamas_mailbox* m) {
+  PeerPush pp{};
+  pp.n = m->world;
+  for (int r = 0; r < m->world; ++r) {
+    pp.keys[r] = reinterpret_cast<uint32_t*>(m->peer[r] + m->keys_off) + (size_t)m->rank * m->n_q * m->budget;
+    pp.flag[r] = reinterpret_cast<uint32_t*>(m->peer[r] + m->kflag_off) + m->rank;
+  }
+  pp.arrive = reinterpret_cast<unsigned int*>(m->base + m->arrive_off);
+  pp.epoch = m->epoch;
+  return pp;
+}
+PeerPush part_push(const adamas_mailbox* m) {
+  PeerPush pp{};
+  pp.n = m->world;
+  for (int r = 0; r < m->world; ++r) {
+    pp.part[r] = reinterpret_cast<float*>(m->peer[r] + m->part_off) + (size_t)m->rank * m->n_q * kPartialStride;
+    pp.flag[r] = reinterpret_cast<uint32_t*>(m->peer[r] + m->pflag_off) + m->rank;
+  }
+  pp.arrive = reinterpret_cast<unsigned int*>(m->base + m->arrive_off) + 32;
+  pp.epoch = m->epoch;
+  return pp;
+}
+int check_mailbox(const adamas_mailbox* m) {
+  if (!m) return fail(ADAMAS_ERR_CONFIG, "null mailbox");
+  for (int r = 0; r < m->world; ++r)
+    if (!m->peer[r]) return fail(ADAMAS_ERR_CONFIG, "mailbox: not connected to every rank");
+  return ADAMAS_OK;
+}
+}  // namespace
+
+int adamas_mailbox_create(adamas_mailbox** out, int rank, int world, int n_q_heads, int64_t budget) {
+  if (!out) return fail(ADAMAS_ERR_CONFIG, "mailbox_create: null out");
+  *out = nullptr;
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return fail(ADAMAS_ERR_CONFIG, "mailbox_create: world must be 1..8 and 0 <= rank < world");
+  if (n_q_heads < 1 || budget < 1 || (int64_t)world * budget > kSelMaxKeys || budget > kSelMaxSurv)
+    return fail(ADAMAS_ERR_CONFIG, "mailbox_create: world * budget must be <= 8192 (budget <= 2048)");
+  auto* m = new adamas_mailbox();
+  m->rank = rank;
+  m->world = world;
+  m->n_q = n_q_heads;
+  m->budget = budget;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  m->keys_off = 0;
+  m->part_off = al((size_t)world * n_q_heads * budget * 4);
+  m->kflag_off = m->part_off + al((size_t)world * n_q_heads * kPartialStride * 4);
+  m->pflag_off = m->kflag_off + 256;
+  m->arrive_off = m->pflag_off + 256;
+  m->bytes = m->arrive_off + 256;
+  if (cudaMalloc(&m->base, m->bytes) != cudaSuccess || cudaMemset(m->base, 0, m->bytes) != cudaSuccess ||
+      cudaMalloc(&m->status, sizeof(int)) != cudaSuccess || cudaMemset(m->status, 0, sizeof(int)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(m->base);
+    cudaFree(m->status);
+    delete m;
+    return fail(ADAMAS_ERR_RUNTIME, "mailbox_create: device allocation failed");
+  }
+  m->peer[rank] = m->base;
+  *out = m;
+  return ADAMAS_OK;
+}
+
+int adamas_mailbox_ipc_handle(const adamas_mailbox* m, void* handle) {
+  if (!m || !handle) return fail(ADAMAS_ERR_CONFIG, "mailbox_ipc_handle: null pointer");
+  cudaIpcMemHandle_t h;
+  ADAMAS_CUDA(cudaIpcGetMemHandle(&h, m->base));
+  std::memcpy(handle, &h, sizeof(h));
+  return ADAMAS_OK;
+}
+
+int adamas_mailbox_connect(adamas_mailbox* m, const void* handles) {
+  if (!m || !handles) return fail(ADAMAS_ERR_CONFIG, "mailbox_connect: null pointer");
+  for (int r = 0; r < m->world; ++r) {
+    if (r == m->rank || m->peer[r]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * ADAMAS_IPC_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    ADAMAS_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    m->peer[r] = static_cast<char*>(ptr);
+    m->ipc_opened[r] = true;
+  }
+  return ADAMAS_OK;
+}
+
+int adamas_mailbox_connect_local(adamas_mailbox* const* boxes, int world) {
+  if (!boxes || world < 1 || world > kMaxPeers) return fail(ADAMAS_ERR_CONFIG, "mailbox_connect_local: bad arguments");
+  for (int i = 0; i < world; ++i) {
+    if (!boxes[i] || boxes[i]->world != world || boxes[i]->rank != i)
+      return fail(ADAMAS_ERR_CONFIG, "mailbox_connect_local: boxes must be ranks 0..world-1 of one world");
+  }
+  for (int i = 0; i < world; ++i)
+    for (int r = 0; r < world; ++r) boxes[i]->peer[r] = boxes[r]->base;
+  return ADAMAS_OK;
+}
+
+int adamas_mailbox_status(adamas_mailbox* m, int* status) {
+  if (!m || !status) return fail(ADAMAS_ERR_CONFIG, "mailbox_status: null pointer");
+  ADAMAS_CUDA(cudaMemcpy(status, m->status, sizeof(int), cudaMemcpyDeviceToHost));
+  return ADAMAS_OK;
+}
+
+int adamas_mailbox_destroy(adamas_mailbox* m) {
+  if (!m) return ADAMAS_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < m->world; ++r)
+    if (m->ipc_opened[r]) cudaIpcCloseMemHandle(m->peer[r]);
+  cudaFree(m->base);
+  cudaFree(m->status);
+  delete m;
+  return ADAMAS_OK;
+}
+
+int adamas_seq_p2p_local(adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, const void* k_new,
+                         const void* v_new, int append, int64_t base_index, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_mailbox(m)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (n_q != m->n_q) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: n_q differs from the mailbox's");
+  if (!q || (append && (!k_new || !v_new))) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: null pointer");
+  if (base_index < 0 || base_index + c->seq_len + (append ? 1 : 0) > (int64_t(1) << 23))
+    return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: global token index must stay below 2^23");
+  if (append && c->seq_len + 1 > c->capacity) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: cache capacity exceeded");
+  cudaStream_t s = as_stream(stream);
+  m->epoch += 1;  // one step: every rank advances in lockstep
+  const PeerPush pp = key_push(m);
+  if (c->seq_len + (append ? 1 : 0) == 0) {  // empty shard: no candidates, still publish
+    peer_empty_keys_kernel<<<1, 256, 0, s>>>(pp, (int64_t)n_q * m->budget);
+    return launch_check("peer_empty_keys_kernel");
+  }
+  adamas_cache* arr[1] = {c};
+  const int rc = fused_decode_launch(arr, 1, c->n_kv, n_q, c->dtype, q, k_new, v_new, m->budget, nullptr, nullptr, s,
+                                     append ? 1 : 0, pp.keys[m->rank], base_index, 0, &pp);
+  if (rc == kFusedUnsupported) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: shape not supported by the fused kernel");
+  if (rc != ADAMAS_OK) return rc;
+  if (append) {
+    c->dirty_from = c->seq_len;
+    c->seq_len += 1;
+  }
+  return ADAMAS_OK;
+}
+
+int adamas_seq_p2p_select_attend(const adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, int64_t total_len,
+                                 int64_t rank_base, int32_t* global_idx, void* stream) {
+  if (int rc = check_cache(c)) return rc;
+  if (int rc = check_mailbox(m)) return rc;
+  if (int rc = check_heads(c, n_q)) return rc;
+  if (n_q != m->n_q || total_len < 1 || !q) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_select_attend: bad arguments");
+  const int k_eff = (int)std::min<int64_t>(m->budget, total_len);
+  const int group = n_q / c->n_kv;
+  const PeerPush pp = part_push(m);
+  const uint32_t* keys = reinterpret_cast<const uint32_t*>(m->base + m->keys_off);
+  const uint32_t* kflags = reinterpret_cast<const uint32_t*>(m->base + m->kflag_off);
+  PeerPush pk = pp;
+  pk.epoch = m->epoch;
+  if (c->dtype == ADAMAS_BF16)
+    seq_select_attend_kernel<__nv_bfloat16><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
+        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, keys,
+        m->world, n_q, m->budget, k_eff, rank_base, c->seq_len, nullptr, global_idx, pk, kflags, m->status);
+  else
+    seq_select_attend_kernel<float><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
+        (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, keys, m->world, n_q, m->budget,
+        k_eff, rank_base, c->seq_len, nullptr, global_idx, pk, kflags, m->status);
+  return launch_check("seq_select_attend_kernel");
+}
+
+int adamas_seq_p2p_merge(adamas_mailbox* m, float* out, void* stream) {
+  if (int rc = check_mailbox(m)) return rc;
+  if (!out) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_merge: null out");
+  const float* parts = reinterpret_cast<const float*>(m->base + m->part_off);
+  const uint32_t* pflags = reinterpret_cast<const uint32_t*>(m->base + m->pflag_off);
+  lse_merge_kernel<<<m->n_q, 32, 0, as_stream(stream)>>>(parts, m->world, m->n_q, out, pflags, m->epoch, m->status);
+  return launch_check("lse_merge_kernel");
+}
+
+int adamas_seq_step_p2p(adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, const void* k_new,
+                        const void* v_new, int append, int64_t base_index, int64_t total_len, float* out,
+                        int32_t* global_idx, void* stream) {
+  if (int rc = adamas_seq_p2p_local(c, m, q, n_q, k_new, v_new, append, base_index, stream)) return rc;
+  if (int rc = adamas_seq_p2p_select_attend(c, m, q, n_q, total_len, base_index, global_idx, stream)) return rc;
+  return adamas_seq_p2p_merge(m, out, stream);
 }
 
 }  // extern "C"

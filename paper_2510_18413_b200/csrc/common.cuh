@@ -29,6 +29,63 @@ constexpr double kQ28 = 0.6744897501960817432;
 // Sticky status bits (C-ABI ADAMAS_STATUS_*).
 constexpr int kStatusDegenerate = 1;  // zero or non-finite vector (quantizer.cpp:46-47)
 constexpr int kStatusSyncTimeout = 4;  // a multi-cluster unit barrier gave up (results invalid)
+constexpr int kStatusPeerTimeout = 8;  // a peer-memory exchange wait gave up (results invalid)
+
+// ---------------------------------------------------------------- peer-memory exchange
+// Sequence-sharded decode exchanges its two small messages (the
+// local candidate keys, the attention partials) by storing straight into every
+// rank's mailbox over NVLink (CUDA IPC mappings) instead of NCCL all-gathers.
+// Each launch's CTAs count themselves in on a local arrival counter; the last
+// one publishes this rank's epoch to every mailbox with a system-scope release;
+// the consumer kernel acquires every rank's epoch before reading.
+constexpr int kMaxPeers = 8;
+
+struct PeerPush {
+  int n;                         // ranks (0: exchange off)
+  uint32_t* keys[kMaxPeers];     // keys mode: this rank's slot in every rank's mailbox
+  float* part[kMaxPeers];        // partials mode: this rank's slot in every rank's mailbox
+  uint32_t* flag[kMaxPeers];     // this rank's flag in every rank's mailbox
+  unsigned int* arrive;          // own mailbox: CTA arrival counter of this launch
+  uint32_t epoch;
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One thread per CTA, after a barrier covering all of the CTA's peer stores.
+__device__ __forceinline__ void peer_signal(const PeerPush& pp) {
+  __threadfence_system();
+  const unsigned old = atomicAdd(pp.arrive, 1u);
+  if (old == gridDim.x * gridDim.y * gridDim.z - 1) {
+    atomicExch(pp.arrive, 0u);  // every CTA of this launch has arrived: reset for the next one
+    __threadfence_system();
+    for (int r = 0; r < pp.n; ++r) st_release_sys(pp.flag[r], pp.epoch);
+  }
+}
+
+// One thread: wait until flags[0..n) all reached `epoch` (wrap-safe compare);
+// gives up after ~4 s and latches kStatusPeerTimeout.
+__device__ __forceinline__ void peer_wait(const uint32_t* flags, int n, uint32_t epoch, int* status) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < n; ++r) {
+    while ((int32_t)(ld_acquire_sys(flags + r) - epoch) < 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 4000000000ull) {
+        atomicOr(status, kStatusPeerTimeout);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+}
 
 struct __align__(32) Code {
   uint32_t lo[4];

@@ -74,6 +74,7 @@ struct FusedParams {
   int append;        // 1: append (k_new, v_new) first (decode step); 0: the cache as is
   uint32_t* cand;    // candidates mode: [n_seqs][n_q][budget] keys (dist << 23 | base + token), no attention
   int64_t cand_base; // global index of this cache's token 0 (sequence-sharded caches)
+  PeerPush peers;    // candidates mode, peer exchange: keys go to every rank's mailbox (cand unused)
   int qsplit;        // clusters per kv-head: each scans the codes for G of its qsplit * G q-heads
   int P;             // clusters per unit (token ranges); > 1 exchanges through global memory
   const void* q;      // [n_seqs][n_q][128]
@@ -630,9 +631,15 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
           const int tok = (int)start + grp * 32 + i;
           if (pos < selcap) sel[g * selcap + pos] = tok;
           if (idx_row) idx_row[pos] = tok;
-          if (p.cand)  // (distance, global index) key: the distributed top-k's order
-            p.cand[((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos] =
-                ((uint32_t)dg[grp * 32 + i] << 23) | (uint32_t)(p.cand_base + tok);
+          if (p.cand) {  // (distance, global index) key: the distributed top-k's order
+            const int64_t off = ((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos;
+            const uint32_t key = ((uint32_t)dg[grp * 32 + i] << 23) | (uint32_t)(p.cand_base + tok);
+            if (p.peers.n) {
+              for (int r = 0; r < p.peers.n; ++r) p.peers.keys[r][off] = key;  // NVLink stores
+            } else {
+              p.cand[off] = key;
+            }
+          }
           ++pos;
         }
       }
@@ -642,13 +649,21 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
     }
     if (gr == 0 && p.cand && t_in == 0) {
-      uint32_t* row = p.cand + ((int64_t)si * n_q + q0 + g) * p.budget;
-      for (int i = k_eff; i < p.budget; ++i) row[i] = 0xffffffffu;
+      const int64_t row = ((int64_t)si * n_q + q0 + g) * p.budget;
+      if (p.peers.n) {
+        for (int r = 0; r < p.peers.n; ++r)
+          for (int i = k_eff; i < p.budget; ++i) p.peers.keys[r][row + i] = 0xffffffffu;
+      } else {
+        for (int i = k_eff; i < p.budget; ++i) p.cand[row + i] = 0xffffffffu;
+      }
     }
   }
   consumer_sync();
   ADAMAS_TRACE(7);
-  if (p.cand) return;  // candidates mode: the selection is the product
+  if (p.cand) {  // candidates mode: the selection is the product
+    if (p.peers.n && tid == 0) peer_signal(p.peers);
+    return;
+  }
 
   // ---------------------------------------------------------------- attend
   {

@@ -429,7 +429,8 @@ __global__ void __launch_bounds__(kSelThreads)
 seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
                          const T* __restrict__ q, const uint32_t* __restrict__ keys, int n_ranks, int n_q,
                          int64_t budget, int k_eff, int64_t rank_base, int64_t rank_len, float* __restrict__ partial,
-                         int32_t* __restrict__ gidx) {
+                         int32_t* __restrict__ gidx, const __grid_constant__ PeerPush push,
+                         const uint32_t* __restrict__ wait_flags, int* __restrict__ status) {
   __shared__ int hist[kSelBins];
   __shared__ int scratch[32];
   __shared__ int s_T, s_below, n_ties, n_surv, n_local;
@@ -446,7 +447,10 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     return keys[((int64_t)r * n_q + h) * budget + i];
   };
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
-  if (tid == 0) { n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0; }
+  if (tid == 0) {
+    n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0;
+    if (push.n) peer_wait(wait_flags, n_ranks, push.epoch, status);  // every rank's keys have landed
+  }
   __syncthreads();
   for (int j = tid; j < n; j += kSelThreads) {
     const uint32_t key = key_at(j);
@@ -506,6 +510,17 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     }
     for (int i = ns + tid; i < budget; i += kSelThreads) gidx[(int64_t)h * budget + i] = -1;
   }
+  // this rank's survivors in ascending order (the atomics above collect them in
+  // arbitrary order; a fixed order makes the fp32 attention deterministic)
+  __syncthreads();
+  int* rows = ties;  // the tie list is no longer needed; nl <= kSelMaxSurv == kSelMaxKeys / 4
+  for (int i = tid; i < nl; i += kSelThreads) {
+    const int v = local_rows[i];
+    int r = 0;
+    for (int j = 0; j < nl; ++j) r += local_rows[j] < v;
+    rows[r] = v;
+  }
+  __syncthreads();
   // attention over this rank's survivors: per-warp online softmax, log2 units
   float qf[4];
   Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)h * kHeadDim + lane * 4), qf);
@@ -516,7 +531,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   const T* Vh = V + (int64_t)hk * cap * kHeadDim + lane * 4;
   float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
   for (int r = warp; r < nl; r += kSelThreads / 32) {
-    const int64_t t = local_rows[r];
+    const int64_t t = rows[r];
     float kf[4], vf[4];
     Raw4<T>::to_float(Raw4<T>::load(Kh + t * kHeadDim), kf);
     Raw4<T>::to_float(Raw4<T>::load(Vh + t * kHeadDim), vf);
@@ -544,20 +559,30 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[j] += wo[w][lane * 4 + j] * c;
     }
-    float* pp = partial + (int64_t)h * kPartialStride;
-    if (lane == 0) {
-      pp[0] = L > 0.f ? M / kLog2e : -INFINITY;  // natural-log units
-      pp[1] = L;
-      pp[2] = 0.f;
-      pp[3] = 0.f;
+    const float4 hdr = make_float4(L > 0.f ? M / kLog2e : -INFINITY, L, 0.f, 0.f);  // natural-log units
+    const float4 body = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    const int nd = push.n ? push.n : 1;
+    for (int r = 0; r < nd; ++r) {  // peer exchange: this rank's partial into every mailbox
+      float* pp = (push.n ? push.part[r] : partial) + (int64_t)h * kPartialStride;
+      if (lane == 0) *reinterpret_cast<float4*>(pp) = hdr;
+      *reinterpret_cast<float4*>(pp + 4 + lane * 4) = body;
     }
-    *reinterpret_cast<float4*>(pp + 4 + lane * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+  if (push.n) {
+    __syncthreads();
+    if (tid == 0) peer_signal(push);
   }
 }
 
 // out[h] = sum_r e^{m_r - M} o_r / sum_r e^{m_r - M} l_r over the ranks' partials.
-__global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks, int n_q, float* __restrict__ out) {
+// With wait_flags, first acquires every rank's partial epoch (peer exchange).
+__global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks, int n_q, float* __restrict__ out,
+                                 const uint32_t* __restrict__ wait_flags, uint32_t epoch, int* __restrict__ status) {
   const int h = blockIdx.x, lane = threadIdx.x;
+  if (wait_flags) {
+    if (lane == 0) peer_wait(wait_flags, n_ranks, epoch, status);
+    __syncwarp();
+  }
   float M = -INFINITY;
   for (int r = 0; r < n_ranks; ++r) {
     const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
@@ -575,6 +600,15 @@ __global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks
   const float inv = L > 0.f ? 1.f / L : 0.f;
   *reinterpret_cast<float4*>(out + (int64_t)h * kHeadDim + lane * 4) =
       make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+}
+
+// An empty shard's candidates: all-empty keys into every mailbox, then the
+// arrival / epoch publication of a one-CTA launch.
+__global__ void peer_empty_keys_kernel(const __grid_constant__ PeerPush push, int64_t n_keys) {
+  for (int r = 0; r < push.n; ++r)
+    for (int64_t i = threadIdx.x; i < n_keys; i += blockDim.x) push.keys[r][i] = 0xffffffffu;
+  __syncthreads();
+  if (threadIdx.x == 0) peer_signal(push);
 }
 
 }  // namespace adamas_dev

@@ -20,6 +20,11 @@ two small collectives between them:
 `SeqShardedDecoder` is the host logic (ranges, bases, tail appends, the phase
 order); the kernels come from `ops` (default: the sm_100a kernels through the
 C ABI) and the collective from `allgather(tensor) -> [world, *shape]`.
+
+Peer-memory exchange (`Mailbox`, `decode_step_p2p`): the same phases with
+both all-gathers replaced by the kernels' own stores into every rank's mailbox
+over NVLink (CUDA IPC mappings) and epoch flags (include/adamas_b200.h,
+"sequence sharding over peer memory"): no NCCL call and no host sync per step.
 """
 from __future__ import annotations
 
@@ -117,6 +122,33 @@ class SeqShardedDecoder:
         return self.ops.lse_merge(partials)
 
     # -- one step with a collective ---------------------------------------------
+    # -- peer-memory exchange ------------------------------------------------------
+    def local_p2p(self, mailbox: Mailbox, q, k_new, v_new, stream=None):
+        append = self.rank == self.tail
+        n_q = q.numel() // HEAD_DIM
+        check(self.ops.L.adamas_seq_p2p_local(self.cache.h, mailbox.h, _ptr(q), n_q, _ptr(k_new if append else None),
+                                              _ptr(v_new if append else None), int(append), self.base,
+                                              _stream(stream)))
+        self.lengths[self.tail] += 1
+
+    def attend_p2p(self, mailbox: Mailbox, q, want_idx=False, stream=None):
+        n_q = q.numel() // HEAD_DIM
+        gidx = torch.empty((n_q, mailbox.budget), dtype=torch.int32, device=q.device) if want_idx else None
+        check(self.ops.L.adamas_seq_p2p_select_attend(self.cache.h, mailbox.h, _ptr(q), n_q, self.total, self.base,
+                                                      _ptr(gidx), _stream(stream)))
+        return gidx
+
+    def merge_p2p(self, mailbox: Mailbox, stream=None):
+        out = torch.empty((mailbox.n_q, HEAD_DIM), dtype=torch.float32, device="cuda")
+        check(self.ops.L.adamas_seq_p2p_merge(mailbox.h, _ptr(out), _stream(stream)))
+        return out
+
+    def decode_step_p2p(self, mailbox: Mailbox, q, k_new, v_new, want_idx=False):
+        """One step over peer memory (every rank calls it; no collective call)."""
+        self.local_p2p(mailbox, q, k_new, v_new)
+        gidx = self.attend_p2p(mailbox, q, want_idx)
+        return self.merge_p2p(mailbox), gidx
+
     def decode_step(self, q, k_new, v_new, budget: int, allgather, want_idx=False):
         """allgather(t) -> tensor [world, *t.shape] in rank order."""
         keys = self.local(q, k_new, v_new, budget)
@@ -124,6 +156,54 @@ class SeqShardedDecoder:
         partial, gidx = self.attend(q, gathered, budget, want_idx)
         partials = allgather(partial)
         return self.merge(partials), gidx
+
+
+class Mailbox:
+    """One rank's mailbox of the peer-memory exchange (adamas_mailbox_*)."""
+
+    HANDLE_BYTES = 64
+
+    def __init__(self, rank: int, world: int, n_q: int, budget: int):
+        self.L = load()
+        self.h = None
+        h = C.c_void_p()
+        check(self.L.adamas_mailbox_create(C.byref(h), rank, world, n_q, budget))
+        self.h, self.rank, self.world, self.n_q, self.budget = h, rank, world, n_q, budget
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(self.HANDLE_BYTES)
+        check(self.L.adamas_mailbox_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def connect(self, handles) -> None:
+        """handles: every rank's ipc_handle(), rank order."""
+        blob = b"".join(handles)
+        check(self.L.adamas_mailbox_connect(self.h, C.create_string_buffer(blob, len(blob))))
+
+    @staticmethod
+    def connect_local(boxes) -> None:
+        arr = (C.c_void_p * len(boxes))(*[b.h for b in boxes])
+        check(load().adamas_mailbox_connect_local(arr, len(boxes)))
+
+    def status(self) -> int:
+        v = C.c_int(0)
+        check(self.L.adamas_mailbox_status(self.h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if self.h:
+            self.L.adamas_mailbox_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+def connect_mailboxes(mailbox: Mailbox, group=None) -> None:
+    """Exchange the IPC handles over torch.distributed (setup only) and map every rank's mailbox."""
+    import torch.distributed as dist
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, mailbox.ipc_handle(), group=group)
+    mailbox.connect(handles)
 
 
 def torch_allgather(group=None):
@@ -138,6 +218,15 @@ def torch_allgather(group=None):
         return out.view(world, *t.shape)
 
     return gather
+
+
+def simulate_step_p2p(decoders, mailboxes, qs, k_new, v_new, want_idx=False):
+    """All ranks of one process over locally connected mailboxes, phase by phase."""
+    for d, m, q in zip(decoders, mailboxes, qs):
+        d.local_p2p(m, q, k_new, v_new)
+    gidx = [d.attend_p2p(m, q, want_idx) for d, m, q in zip(decoders, mailboxes, qs)]
+    outs = [d.merge_p2p(m) for d, m in zip(decoders, mailboxes)]
+    return outs, gidx
 
 
 def simulate_step(decoders, qs, k_new, v_new, budget: int, want_idx=False):
