@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=11)
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="seqshard1m at N > 1: peer-memory mailboxes (default) or NCCL all-gathers")
     a = ap.parse_args()
     for k, v in CONFIGS.get(a.config, {}).items():
         if getattr(a, k) is None:
@@ -249,9 +251,17 @@ def run_ours(args):
     import paper_2510_18413_b200 as ad
 
     ws, rank, local = dist_setup()
+    # protocol checks of the N > 1 paths on a one-GPU box (never for numbers):
+    # ADAMAS_BENCH_SAME_DEVICE=1 puts every rank on cuda:0, ADAMAS_BENCH_BACKEND=gloo
+    if os.environ.get("ADAMAS_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("ADAMAS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     seqshard = args.config == "seqshard1m"
     if not seqshard and (args.heads % ws or args.kv_heads % ws):
         raise SystemExit("heads must divide across ranks")
@@ -277,37 +287,56 @@ def run_ours(args):
     idx = torch.empty((L, NS, n_q, B), dtype=torch.int32, device="cuda")
 
     if seqshard:
-        # one rank's share of the 8-way split: ranks r < 8 own [r S, (r + 1) S);
-        # this process is rank `rank` of the world, the other shards' keys come
-        # from the all-gather (N > 1) or are synthesized from this shard's keys
-        # with shifted indices (N = 1, the per-GPU work of the 8-GPU job).
-        from paper_2510_18413_b200.seqshard import CudaSeqOps, torch_allgather
+        # N = 1: one rank's share of the 8-way split (the other shards' keys
+        # are synthesized from this shard's keys with shifted indices, one
+        # kernel). N > 1: a world-way split of an N x S context, rank r owning
+        # [r S, (r + 1) S); the two exchanges go through peer memory (the
+        # kernels store into every rank's CUDA-IPC mailbox, --exchange p2p,
+        # default) or NCCL all-gathers (--exchange nccl).
+        from paper_2510_18413_b200.seqshard import CudaSeqOps, Mailbox, connect_mailboxes, torch_allgather
         ops = CudaSeqOps()
-        n_virtual = 8
-        gather = torch_allgather() if ws > 1 else None
-        keys_all = torch.empty((L, n_virtual, n_q, B), dtype=torch.int32, device="cuda")
-        parts_all = torch.empty((L, n_virtual, n_q, 132), dtype=torch.float32, device="cuda")
+        n_virtual = 8 if ws == 1 else ws
         my_slot = rank % n_virtual
         base = my_slot * S
-        shard_off = ((torch.arange(n_virtual, device="cuda", dtype=torch.int32) - my_slot) * S).view(-1, 1, 1)
+        tail = my_slot == n_virtual - 1
+        if ws > 1 and args.exchange == "p2p":
+            mbox = Mailbox(rank, ws, n_q, B)
+            connect_mailboxes(mbox)
+            Lh = ops.L
+            from paper_2510_18413_b200.seqshard import _ptr, _stream
 
-        def step(s, st):
-            for l in range(L):
-                c = caches[l][0]
-                keys = ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], my_slot == n_virtual - 1,
-                                            base, B, stream=st)
-                if gather is not None:
-                    keys_all[l, :ws].copy_(gather(keys))
-                else:  # other shards: same distances, indices moved to their ranges (one kernel)
-                    torch.add(keys.unsqueeze(0), shard_off, out=keys_all[l])
-                part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
-                if gather is not None:
-                    parts_all[l, :ws].copy_(gather(part))
-                else:
-                    parts_all[l].copy_(part.unsqueeze(0).expand(n_virtual, -1, -1))
-                out[l, 0].copy_(ops.lse_merge(parts_all[l], stream=st))
-                if my_slot == n_virtual - 1:
-                    c.truncate(S - 1)
+            def step(s, st):
+                for l in range(L):
+                    c = caches[l][0]
+                    rc = Lh.adamas_seq_step_p2p(c.h, mbox.h, _ptr(qs[s, l, 0]), n_q, _ptr(ks[s, l, 0]),
+                                                _ptr(vs[s, l, 0]), int(tail), base, n_virtual * S, _ptr(out[l, 0]),
+                                                None, _stream(st))
+                    if rc:
+                        raise RuntimeError(Lh.adamas_last_error().decode())
+                    if tail:
+                        c.truncate(S - 1)
+        else:
+            gather = torch_allgather() if ws > 1 else None
+            keys_all = torch.empty((L, n_virtual, n_q, B), dtype=torch.int32, device="cuda")
+            parts_all = torch.empty((L, n_virtual, n_q, 132), dtype=torch.float32, device="cuda")
+            shard_off = ((torch.arange(n_virtual, device="cuda", dtype=torch.int32) - my_slot) * S).view(-1, 1, 1)
+
+            def step(s, st):
+                for l in range(L):
+                    c = caches[l][0]
+                    keys = ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], tail, base, B, stream=st)
+                    if gather is not None:
+                        keys_all[l].copy_(gather(keys))
+                    else:  # other shards: same distances, indices moved to their ranges (one kernel)
+                        torch.add(keys.unsqueeze(0), shard_off, out=keys_all[l])
+                    part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
+                    if gather is not None:
+                        parts_all[l].copy_(gather(part))
+                    else:
+                        parts_all[l].copy_(part.unsqueeze(0).expand(n_virtual, -1, -1))
+                    out[l, 0].copy_(ops.lse_merge(parts_all[l], stream=st))
+                    if tail:
+                        c.truncate(S - 1)
     else:
         def step(s, st):
             for l in range(L):
@@ -427,12 +456,14 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        par = (f"sequence-shard x8 (rank {my_slot} of the split, world {ws})" if seqshard
+        par = (f"sequence-shard x{n_virtual} (rank {my_slot} of the split, world {ws}"
+               + (f", {args.exchange} exchange)" if ws > 1 else ", other shards synthesized)") if seqshard
                else f"head-shard x{ws}")
         line = {
             "metric": METRIC, "value": us_per_token_layer, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "scaling": "weak" if seqshard else "strong", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config].format(**vars(args)) + f", {args.dtype} K/V, "
                                    f"{L} layers per step",
                        "name": args.config, "layers_per_step": L, "sequences": NS, "heads_per_rank": n_q,

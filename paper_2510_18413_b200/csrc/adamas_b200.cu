@@ -392,7 +392,6 @@ struct adamas_mailbox {
   char* base = nullptr;                 // own mailbox (cudaMalloc: IPC-exportable)
   char* peer[kMaxPeers] = {};           // every rank's mailbox as mapped here (peer[rank] = base)
   bool ipc_opened[kMaxPeers] = {};
-  uint32_t epoch = 0;
   int* status = nullptr;
 };
 
@@ -1198,7 +1197,8 @@ PeerPush key_push(const adamas_mailbox* m) {
     pp.flag[r] = reinterpret_cast<uint32_t*>(m->peer[r] + m->kflag_off) + m->rank;
   }
   pp.arrive = reinterpret_cast<unsigned int*>(m->base + m->arrive_off);
-  pp.epoch = m->epoch;
+  pp.epoch = reinterpret_cast<uint32_t*>(m->base + m->arrive_off) + 64;
+  pp.bump = 1;
   return pp;
 }
 PeerPush part_push(const adamas_mailbox* m) {
@@ -1209,7 +1209,8 @@ PeerPush part_push(const adamas_mailbox* m) {
     pp.flag[r] = reinterpret_cast<uint32_t*>(m->peer[r] + m->pflag_off) + m->rank;
   }
   pp.arrive = reinterpret_cast<unsigned int*>(m->base + m->arrive_off) + 32;
-  pp.epoch = m->epoch;
+  pp.epoch = reinterpret_cast<uint32_t*>(m->base + m->arrive_off) + 64;
+  pp.bump = 0;
   return pp;
 }
 int check_mailbox(const adamas_mailbox* m) {
@@ -1238,7 +1239,7 @@ int adamas_mailbox_create(adamas_mailbox** out, int rank, int world, int n_q_hea
   m->kflag_off = m->part_off + al((size_t)world * n_q_heads * kPartialStride * 4);
   m->pflag_off = m->kflag_off + 256;
   m->arrive_off = m->pflag_off + 256;
-  m->bytes = m->arrive_off + 256;
+  m->bytes = m->arrive_off + 512;  // arrive[0] keys, arrive[32] partials, [64] step epoch
   if (cudaMalloc(&m->base, m->bytes) != cudaSuccess || cudaMemset(m->base, 0, m->bytes) != cudaSuccess ||
       cudaMalloc(&m->status, sizeof(int)) != cudaSuccess || cudaMemset(m->status, 0, sizeof(int)) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {
@@ -1313,8 +1314,7 @@ int adamas_seq_p2p_local(adamas_cache* c, adamas_mailbox* m, const void* q, int 
     return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: global token index must stay below 2^23");
   if (append && c->seq_len + 1 > c->capacity) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_local: cache capacity exceeded");
   cudaStream_t s = as_stream(stream);
-  m->epoch += 1;  // one step: every rank advances in lockstep
-  const PeerPush pp = key_push(m);
+  const PeerPush pp = key_push(m);  // the launch's last CTA advances the device-side step epoch
   if (c->seq_len + (append ? 1 : 0) == 0) {  // empty shard: no candidates, still publish
     peer_empty_keys_kernel<<<1, 256, 0, s>>>(pp, (int64_t)n_q * m->budget);
     return launch_check("peer_empty_keys_kernel");
@@ -1342,8 +1342,7 @@ int adamas_seq_p2p_select_attend(const adamas_cache* c, adamas_mailbox* m, const
   const PeerPush pp = part_push(m);
   const uint32_t* keys = reinterpret_cast<const uint32_t*>(m->base + m->keys_off);
   const uint32_t* kflags = reinterpret_cast<const uint32_t*>(m->base + m->kflag_off);
-  PeerPush pk = pp;
-  pk.epoch = m->epoch;
+  const PeerPush& pk = pp;
   if (c->dtype == ADAMAS_BF16)
     seq_select_attend_kernel<__nv_bfloat16><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
         (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, keys,
@@ -1360,7 +1359,8 @@ int adamas_seq_p2p_merge(adamas_mailbox* m, float* out, void* stream) {
   if (!out) return fail(ADAMAS_ERR_CONFIG, "seq_p2p_merge: null out");
   const float* parts = reinterpret_cast<const float*>(m->base + m->part_off);
   const uint32_t* pflags = reinterpret_cast<const uint32_t*>(m->base + m->pflag_off);
-  lse_merge_kernel<<<m->n_q, 32, 0, as_stream(stream)>>>(parts, m->world, m->n_q, out, pflags, m->epoch, m->status);
+  const uint32_t* epoch = reinterpret_cast<const uint32_t*>(m->base + m->arrive_off) + 64;
+  lse_merge_kernel<<<m->n_q, 32, 0, as_stream(stream)>>>(parts, m->world, m->n_q, out, pflags, epoch, m->status);
   return launch_check("lse_merge_kernel");
 }
 

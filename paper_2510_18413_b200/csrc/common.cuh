@@ -46,7 +46,8 @@ struct PeerPush {
   float* part[kMaxPeers];        // partials mode: this rank's slot in every rank's mailbox
   uint32_t* flag[kMaxPeers];     // this rank's flag in every rank's mailbox
   unsigned int* arrive;          // own mailbox: CTA arrival counter of this launch
-  uint32_t epoch;
+  uint32_t* epoch;               // own mailbox: this rank's step counter (device-side: graph replays advance it)
+  int bump;                      // 1: this launch starts a new step (keys phase)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -64,14 +65,18 @@ __device__ __forceinline__ void peer_signal(const PeerPush& pp) {
   const unsigned old = atomicAdd(pp.arrive, 1u);
   if (old == gridDim.x * gridDim.y * gridDim.z - 1) {
     atomicExch(pp.arrive, 0u);  // every CTA of this launch has arrived: reset for the next one
+    const uint32_t e = *(volatile uint32_t*)pp.epoch + (pp.bump ? 1u : 0u);
+    if (pp.bump) *(volatile uint32_t*)pp.epoch = e;
     __threadfence_system();
-    for (int r = 0; r < pp.n; ++r) st_release_sys(pp.flag[r], pp.epoch);
+    for (int r = 0; r < pp.n; ++r) st_release_sys(pp.flag[r], e);
   }
 }
 
-// One thread: wait until flags[0..n) all reached `epoch` (wrap-safe compare);
-// gives up after ~4 s and latches kStatusPeerTimeout.
-__device__ __forceinline__ void peer_wait(const uint32_t* flags, int n, uint32_t epoch, int* status) {
+// One thread: wait until flags[0..n) all reached this rank's current step
+// (*epoch_ctr, bumped by the step's keys launch; wrap-safe compare); gives up
+// after ~4 s and latches kStatusPeerTimeout.
+__device__ __forceinline__ void peer_wait(const uint32_t* flags, int n, const uint32_t* epoch_ctr, int* status) {
+  const uint32_t epoch = *(const volatile uint32_t*)epoch_ctr;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int r = 0; r < n; ++r) {

@@ -449,7 +449,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
   if (tid == 0) {
     n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0;
-    if (push.n) peer_wait(wait_flags, n_ranks, push.epoch, status);  // every rank's keys have landed
+    if (push.n) peer_wait(wait_flags, n_ranks, push.epoch, status);  // every rank's keys of this step have landed
   }
   __syncthreads();
   for (int j = tid; j < n; j += kSelThreads) {
@@ -577,7 +577,8 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
 // out[h] = sum_r e^{m_r - M} o_r / sum_r e^{m_r - M} l_r over the ranks' partials.
 // With wait_flags, first acquires every rank's partial epoch (peer exchange).
 __global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks, int n_q, float* __restrict__ out,
-                                 const uint32_t* __restrict__ wait_flags, uint32_t epoch, int* __restrict__ status) {
+                                 const uint32_t* __restrict__ wait_flags, const uint32_t* __restrict__ epoch,
+                                 int* __restrict__ status) {
   const int h = blockIdx.x, lane = threadIdx.x;
   if (wait_flags) {
     if (lane == 0) peer_wait(wait_flags, n_ranks, epoch, status);
