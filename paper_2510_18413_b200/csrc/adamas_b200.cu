@@ -243,8 +243,16 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
         const int c = fused_decode_launch(caches, n_seqs, n_kv, n_q, dtype, q, k_new, v_new, budget, out, idx, s,
                                           append, cand, cand_base, -qs);  // probe: C with this split
         if (c == kFusedUnsupported) continue;
-        if (c <= 4) { best = qs; break; }
+        if (c <= 4) { best = qs; best_c = c; break; }
         if (c < best_c) { best = qs; best_c = c; }
+      }
+      // More than one wave of CTAs: splitting the q-heads beats splitting the
+      // tokens at the same CTA count (measured: 16 x 32K Llama batch, qsplit 1
+      // x C 2 101 us vs qsplit 2 x C 1 87 us per layer-step).
+      if (best_c > 1 && (int64_t)n_seqs * n_kv * best * best_c > sm_count() && G_all % (2 * best) == 0) {
+        const int c2 = fused_decode_launch(caches, n_seqs, n_kv, n_q, dtype, q, k_new, v_new, budget, out, idx, s,
+                                           append, cand, cand_base, -2 * best);
+        if (c2 != kFusedUnsupported && c2 < best_c) best *= 2;
       }
       qsplit = best;
     }
