@@ -492,6 +492,37 @@ int pool_grow(void** p, size_t* have, size_t need, cudaStream_t s) {
   return ADAMAS_OK;
 }
 
+// dynamic shared memory of seq_select_attend_kernel: the q-head's keys
+size_t sel_smem(int n_ranks, int64_t budget) {
+  static bool init = false;
+  if (!init) {  // up to kSelMaxKeys keys (32 KB) on top of ~29 KB static
+    cudaFuncSetAttribute(seq_select_attend_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSelMaxKeys * 4);
+    cudaFuncSetAttribute(seq_select_attend_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSelMaxKeys * 4);
+    init = true;
+  }
+  return (size_t)n_ranks * budget * sizeof(uint32_t);
+}
+
+// Launch with programmatic stream serialization (PDL) unless ADAMAS_NO_PDL:
+// the kernel's griddepcontrol.wait orders it after its predecessor, while its
+// launch and prologue overlap the predecessor's tail.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int check_rows(int64_t n_rows, int64_t rows_per_inst, int64_t n_inst) {
   if (n_rows < 0 || rows_per_inst < 1) return fail(ADAMAS_ERR_CONFIG, "rows: bad row count / rows_per_inst");
   if (n_rows > 0 && (n_rows - 1) / rows_per_inst >= n_inst)
@@ -807,20 +838,26 @@ int adamas_seq_select_attend(const adamas_cache* c, const void* q, int n_q, cons
   const int k_eff = (int)std::min<int64_t>(budget, total_len);
   const int group = n_q / c->n_kv;
   if (c->dtype == ADAMAS_BF16)
-    seq_select_attend_kernel<__nv_bfloat16><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
-        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, gathered,
-        n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{}, nullptr, c->status);
+    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<__nv_bfloat16>, dim3(n_q), dim3(kSelThreads),
+                           sel_smem(n_ranks, budget), as_stream(stream), (const __nv_bfloat16*)c->K,
+                           (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, gathered, n_ranks,
+                           n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{},
+                           (const uint32_t*)nullptr, c->status, (const float*)nullptr, (const uint32_t*)nullptr,
+                           (float*)nullptr));
   else
-    seq_select_attend_kernel<float><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
-        (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, gathered, n_ranks, n_q, budget,
-        k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{}, nullptr, c->status);
+    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<float>, dim3(n_q), dim3(kSelThreads), sel_smem(n_ranks, budget),
+                           as_stream(stream), (const float*)c->K, (const float*)c->V, c->capacity, group,
+                           (const float*)q, gathered, n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial,
+                           global_idx, PeerPush{}, (const uint32_t*)nullptr, c->status, (const float*)nullptr,
+                           (const uint32_t*)nullptr, (float*)nullptr));
   return launch_check("seq_select_attend_kernel");
 }
 
 int adamas_lse_merge(const float* partials, int n_ranks, int n_q, float* out, void* stream) {
   if (n_ranks < 1 || n_q < 1) return fail(ADAMAS_ERR_CONFIG, "lse_merge: bad sizes");
   if (!partials || !out) return fail(ADAMAS_ERR_CONFIG, "lse_merge: null pointer");
-  lse_merge_kernel<<<n_q, 32, 0, as_stream(stream)>>>(partials, n_ranks, n_q, out, nullptr, 0, nullptr);
+  ADAMAS_CUDA(launch_pdl(lse_merge_kernel, dim3(n_q), dim3(32), 0, as_stream(stream), partials, n_ranks, n_q, out,
+                         (const uint32_t*)nullptr, (const uint32_t*)nullptr, (int*)nullptr));
   return launch_check("lse_merge_kernel");
 }
 
@@ -1339,8 +1376,9 @@ int adamas_seq_p2p_local(adamas_cache* c, adamas_mailbox* m, const void* q, int 
   return ADAMAS_OK;
 }
 
-int adamas_seq_p2p_select_attend(const adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, int64_t total_len,
-                                 int64_t rank_base, int32_t* global_idx, void* stream) {
+namespace {
+int p2p_select_attend(const adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, int64_t total_len,
+                      int64_t rank_base, int32_t* global_idx, float* merge_out, void* stream) {
   if (int rc = check_cache(c)) return rc;
   if (int rc = check_mailbox(m)) return rc;
   if (int rc = check_heads(c, n_q)) return rc;
@@ -1351,15 +1389,30 @@ int adamas_seq_p2p_select_attend(const adamas_cache* c, adamas_mailbox* m, const
   const uint32_t* keys = reinterpret_cast<const uint32_t*>(m->base + m->keys_off);
   const uint32_t* kflags = reinterpret_cast<const uint32_t*>(m->base + m->kflag_off);
   const PeerPush& pk = pp;
+  // merge_out: the merge runs in the same launch (one CTA per q-head, all resident)
+  const float* parts = reinterpret_cast<const float*>(m->base + m->part_off);
+  const uint32_t* pflags = reinterpret_cast<const uint32_t*>(m->base + m->pflag_off);
+  const size_t dyn = sel_smem(m->world, m->budget);
+  const float* mp = merge_out ? parts : nullptr;
+  const uint32_t* mf = merge_out ? pflags : nullptr;
   if (c->dtype == ADAMAS_BF16)
-    seq_select_attend_kernel<__nv_bfloat16><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
-        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, keys,
-        m->world, n_q, m->budget, k_eff, rank_base, c->seq_len, nullptr, global_idx, pk, kflags, m->status);
+    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<__nv_bfloat16>, dim3(n_q), dim3(kSelThreads), dyn,
+                           as_stream(stream), (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity,
+                           group, (const __nv_bfloat16*)q, keys, m->world, n_q, m->budget, k_eff, rank_base,
+                           c->seq_len, (float*)nullptr, global_idx, pk, kflags, m->status, mp, mf, merge_out));
   else
-    seq_select_attend_kernel<float><<<n_q, kSelThreads, 0, as_stream(stream)>>>(
-        (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, keys, m->world, n_q, m->budget,
-        k_eff, rank_base, c->seq_len, nullptr, global_idx, pk, kflags, m->status);
+    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<float>, dim3(n_q), dim3(kSelThreads), dyn, as_stream(stream),
+                           (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, keys, m->world,
+                           n_q, m->budget, k_eff, rank_base, c->seq_len, (float*)nullptr, global_idx, pk, kflags,
+                           m->status, mp, mf, merge_out));
   return launch_check("seq_select_attend_kernel");
+}
+
+}  // namespace
+
+int adamas_seq_p2p_select_attend(const adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, int64_t total_len,
+                                 int64_t rank_base, int32_t* global_idx, void* stream) {
+  return p2p_select_attend(c, m, q, n_q, total_len, rank_base, global_idx, nullptr, stream);
 }
 
 int adamas_seq_p2p_merge(adamas_mailbox* m, float* out, void* stream) {
@@ -1368,14 +1421,18 @@ int adamas_seq_p2p_merge(adamas_mailbox* m, float* out, void* stream) {
   const float* parts = reinterpret_cast<const float*>(m->base + m->part_off);
   const uint32_t* pflags = reinterpret_cast<const uint32_t*>(m->base + m->pflag_off);
   const uint32_t* epoch = reinterpret_cast<const uint32_t*>(m->base + m->arrive_off) + 64;
-  lse_merge_kernel<<<m->n_q, 32, 0, as_stream(stream)>>>(parts, m->world, m->n_q, out, pflags, epoch, m->status);
+  ADAMAS_CUDA(launch_pdl(lse_merge_kernel, dim3(m->n_q), dim3(32), 0, as_stream(stream), parts, m->world, m->n_q, out,
+                         pflags, epoch, m->status));
   return launch_check("lse_merge_kernel");
 }
 
 int adamas_seq_step_p2p(adamas_cache* c, adamas_mailbox* m, const void* q, int n_q, const void* k_new,
                         const void* v_new, int append, int64_t base_index, int64_t total_len, float* out,
                         int32_t* global_idx, void* stream) {
+  if (!out) return fail(ADAMAS_ERR_CONFIG, "seq_step_p2p: null out");
   if (int rc = adamas_seq_p2p_local(c, m, q, n_q, k_new, v_new, append, base_index, stream)) return rc;
+  if (n_q <= sm_count())  // every select CTA resident: merge in the same launch
+    return p2p_select_attend(c, m, q, n_q, total_len, base_index, global_idx, out, stream);
   if (int rc = adamas_seq_p2p_select_attend(c, m, q, n_q, total_len, base_index, global_idx, stream)) return rc;
   return adamas_seq_p2p_merge(m, out, stream);
 }

@@ -430,7 +430,10 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
                          const T* __restrict__ q, const uint32_t* __restrict__ keys, int n_ranks, int n_q,
                          int64_t budget, int k_eff, int64_t rank_base, int64_t rank_len, float* __restrict__ partial,
                          int32_t* __restrict__ gidx, const __grid_constant__ PeerPush push,
-                         const uint32_t* __restrict__ wait_flags, int* __restrict__ status) {
+                         const uint32_t* __restrict__ wait_flags, int* __restrict__ status,
+                         const float* __restrict__ merge_parts, const uint32_t* __restrict__ merge_flags,
+                         float* __restrict__ merge_out) {
+  extern __shared__ uint32_t skeys[];  // the n_ranks * budget keys of this q-head, read once
   __shared__ int hist[kSelBins];
   __shared__ int scratch[32];
   __shared__ int s_T, s_below, n_ties, n_surv, n_local;
@@ -442,10 +445,11 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   const int h = blockIdx.x, hk = h / group;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = n_ranks * (int)budget;
-  auto key_at = [&](int j) {  // j = r * budget + i
-    const int r = j / (int)budget, i = j - r * (int)budget;
-    return keys[((int64_t)r * n_q + h) * budget + i];
-  };
+  auto key_at = [&](int j) { return skeys[j]; };  // j = r * budget + i
+  // programmatic dependent launch: keys / the appended row come from the
+  // preceding kernel; the next launch may begin its own prologue now
+  grid_dependency_wait();
+  if (tid == 0) grid_launch_dependents();
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
   if (tid == 0) {
     n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0;
@@ -453,7 +457,9 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   }
   __syncthreads();
   for (int j = tid; j < n; j += kSelThreads) {
-    const uint32_t key = key_at(j);
+    const int r = j / (int)budget, i = j - r * (int)budget;
+    const uint32_t key = keys[((int64_t)r * n_q + h) * budget + i];
+    skeys[j] = key;
     if (key != 0xffffffffu) atomicAdd(&hist[key >> 23], 1);
   }
   __syncthreads();
@@ -572,6 +578,29 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     __syncthreads();
     if (tid == 0) peer_signal(push);
   }
+  if (merge_out) {  // fused log-sum-exp merge of this q-head (every CTA of the launch is resident)
+    if (tid == 0) peer_wait(merge_flags, n_ranks, push.epoch, status);
+    __syncthreads();
+    if (warp == 0) {
+      float M = -INFINITY;
+      for (int r = 0; r < n_ranks; ++r) {
+        const float* pp = merge_parts + ((int64_t)r * n_q + h) * kPartialStride;
+        if (pp[1] > 0.f) M = fmaxf(M, pp[0]);
+      }
+      float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int r = 0; r < n_ranks; ++r) {
+        const float* pp = merge_parts + ((int64_t)r * n_q + h) * kPartialStride;
+        if (!(pp[1] > 0.f)) continue;
+        const float c = __expf(pp[0] - M);
+        L += pp[1] * c;
+        const float4 v = *reinterpret_cast<const float4*>(pp + 4 + lane * 4);
+        acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
+      }
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      *reinterpret_cast<float4*>(merge_out + (int64_t)h * kHeadDim + lane * 4) =
+          make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    }
+  }
 }
 
 // out[h] = sum_r e^{m_r - M} o_r / sum_r e^{m_r - M} l_r over the ranks' partials.
@@ -580,6 +609,8 @@ __global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks
                                  const uint32_t* __restrict__ wait_flags, const uint32_t* __restrict__ epoch,
                                  int* __restrict__ status) {
   const int h = blockIdx.x, lane = threadIdx.x;
+  grid_dependency_wait();  // partials come from the preceding kernel (PDL launch)
+  if (lane == 0) grid_launch_dependents();
   if (wait_flags) {
     if (lane == 0) peer_wait(wait_flags, n_ranks, epoch, status);
     __syncwarp();

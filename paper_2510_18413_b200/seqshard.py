@@ -143,11 +143,21 @@ class SeqShardedDecoder:
         check(self.ops.L.adamas_seq_p2p_merge(mailbox.h, _ptr(out), _stream(stream)))
         return out
 
-    def decode_step_p2p(self, mailbox: Mailbox, q, k_new, v_new, want_idx=False):
-        """One step over peer memory (every rank calls it; no collective call)."""
-        self.local_p2p(mailbox, q, k_new, v_new)
-        gidx = self.attend_p2p(mailbox, q, want_idx)
-        return self.merge_p2p(mailbox), gidx
+    def decode_step_p2p(self, mailbox: Mailbox, q, k_new, v_new, want_idx=False, stream=None):
+        """One step over peer memory (every rank calls it; no collective call):
+        adamas_seq_step_p2p, whose select/attend launch also does the merge.
+        Ranks must run concurrently (one per GPU / process); ranks simulated
+        in one stream use simulate_step_p2p's phase-by-phase order instead."""
+        append = self.rank == self.tail
+        n_q = q.numel() // HEAD_DIM
+        out = torch.empty((n_q, HEAD_DIM), dtype=torch.float32, device=q.device)
+        gidx = torch.empty((n_q, mailbox.budget), dtype=torch.int32, device=q.device) if want_idx else None
+        total = self.total + 1  # after this step's append
+        check(self.ops.L.adamas_seq_step_p2p(self.cache.h, mailbox.h, _ptr(q), n_q, _ptr(k_new if append else None),
+                                             _ptr(v_new if append else None), int(append), self.base, total,
+                                             _ptr(out), _ptr(gidx), _stream(stream)))
+        self.lengths[self.tail] += 1
+        return out, gidx
 
     def decode_step(self, q, k_new, v_new, budget: int, allgather, want_idx=False):
         """allgather(t) -> tensor [world, *t.shape] in rank order."""
