@@ -125,3 +125,22 @@ def test_seq_sharded_peer_exchange_two_processes(gpu, tmp_path):
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     for r in range(2):
         assert (tmp_path / f"ok{r}").read_text() == "ok", r
+
+
+def test_mailbox_errors(gpu):
+    from paper_2510_18413_b200._lib import ConfigError
+    from paper_2510_18413_b200.seqshard import Mailbox, SeqShardedDecoder
+    with pytest.raises(ConfigError):
+        Mailbox(2, 2, 4, 128)          # rank out of range
+    with pytest.raises(ConfigError):
+        Mailbox(0, 9, 4, 128)          # more than 8 ranks
+    with pytest.raises(ConfigError):
+        Mailbox(0, 8, 4, 2048)         # world * budget > 8192
+    box = Mailbox(0, 2, 4, 64)         # peer 1 never connected
+    c = gpu.KvCache(1, 64, torch.bfloat16)
+    c.update(torch.randn(32, 1, 128, device="cuda").bfloat16(), torch.randn(32, 1, 128, device="cuda").bfloat16())
+    dec = SeqShardedDecoder(c, 0, 2, [32, 32])
+    q = torch.randn(4, 128, device="cuda").bfloat16()
+    with pytest.raises(ConfigError, match="not connected"):
+        dec.local_p2p(box, q, None, None)
+    assert len(box.ipc_handle()) == Mailbox.HANDLE_BYTES
