@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <fstream>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -462,20 +463,24 @@ int hsel_status_check(int* status, cudaStream_t s) {
 // the driver at every synchronisation, and re-mapping 100 MB buffers costs
 // milliseconds per call).
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
-  if (!pools[dev]) {
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    cudaMemPool_t pool;
-    if (cudaError_t e = cudaMemPoolCreate(&pool, &props)) return e;
-    uint64_t keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    pools[dev] = pool;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t pool;
+      if (cudaError_t e = cudaMemPoolCreate(&pool, &props)) return e;
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = pool;
+    }
   }
   return cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 8), pools[dev], s);
 }
@@ -494,14 +499,14 @@ int pool_grow(void** p, size_t* have, size_t need, cudaStream_t s) {
 
 // dynamic shared memory of seq_select_attend_kernel: the q-head's keys
 size_t sel_smem(int n_ranks, int64_t budget) {
-  static bool init = false;
-  if (!init) {  // up to kSelMaxKeys keys (32 KB) on top of ~29 KB static
+  static const bool init = [] {  // up to kSelMaxKeys keys (32 KB) on top of ~29 KB static
     cudaFuncSetAttribute(seq_select_attend_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSelMaxKeys * 4);
     cudaFuncSetAttribute(seq_select_attend_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSelMaxKeys * 4);
-    init = true;
-  }
+    return true;
+  }();
+  (void)init;
   return (size_t)n_ranks * budget * sizeof(uint32_t);
 }
 
@@ -519,7 +524,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
+  static const bool no_pdl = env_int("ADAMAS_NO_PDL", 0) != 0;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
@@ -1074,8 +1080,25 @@ int adamas_hsel_select(adamas_hsel* h, const double* queries, int64_t n_rows, in
   if (budget < 0) return fail(ADAMAS_ERR_CONFIG, "hsel_select: negative budget");
   if (int rc = check_rows(n_rows, rows_per_inst, h->n_inst)) return rc;
   if (n_rows == 0) return ADAMAS_OK;
-  if (n_rows > 65535) return fail(ADAMAS_ERR_CONFIG, "hsel_select: at most 65535 query rows per call");
   if (!queries || (budget > 0 && !idx)) return fail(ADAMAS_ERR_CONFIG, "hsel_select: null pointer");
+  // grid.y limit: chunks of whole instances
+  const int64_t step = std::max<int64_t>(1, 32768 / rows_per_inst) * rows_per_inst;
+  if (std::min(step, n_rows) > 65535) return fail(ADAMAS_ERR_CONFIG, "hsel_select: more than 65535 rows per instance");
+  if (step < n_rows) {
+    for (int64_t r0 = 0; r0 < n_rows; r0 += step) {
+      adamas_hsel sub = *h;  // same codes, shifted instance window; own scratch below
+      const int64_t inst0 = r0 / rows_per_inst;
+      sub.n_inst = h->n_inst - inst0;
+      const size_t cb = hsel_code_bytes(h->head_dim, h->bits) / (h->bits == 3 ? 1 : sizeof(uint32_t));
+      if (h->planes) sub.planes = h->planes + (size_t)inst0 * h->seq_len * cb;
+      if (h->bytes) sub.bytes = h->bytes + (size_t)inst0 * h->seq_len * cb;
+      const int rc = adamas_hsel_select(&sub, queries + r0 * h->head_dim, std::min(step, n_rows - r0), rows_per_inst,
+                                        metric, budget, idx + r0 * budget, stream);
+      h->qcodes = sub.qcodes; h->q_cap = sub.q_cap; h->scores = sub.scores; h->scores_cap = sub.scores_cap;
+      if (rc) return rc;
+    }
+    return ADAMAS_OK;
+  }
   cudaStream_t s = as_stream(stream);
   const int D = h->head_dim;
   if (int rc = pool_grow(&h->qcodes, &h->q_cap, (size_t)n_rows * hsel_code_bytes(D, h->bits), s)) return rc;

@@ -251,3 +251,16 @@ def test_acceptance_needle_criterion(gpu, reference):
     csv, _, nd = reference.run_sweep(spec, sweep)
     assert H.rows_to_csv(rows) == csv
     assert H.needle_summary_to_csv(H.needle_report(rows)) == nd
+
+
+def test_select_many_rows_chunked(gpu, reference):
+    """More query rows than one launch's grid holds: chunks of whole instances."""
+    d, S, n_inst, rpi = 16, 40, 700, 100  # 70000 rows
+    rng = np.random.default_rng(77)
+    K = rng.standard_normal((n_inst, S, d))
+    Q = rng.standard_normal((n_inst * rpi, d))
+    sel = H.HarnessSelector(d, 2, True)
+    sel.build(torch.as_tensor(K, device="cuda"))
+    got = sel.select(torch.as_tensor(Q, device="cuda"), 5, "l1", rows_per_inst=rpi).cpu().numpy()
+    for r in [0, 1, 32767, 32768, 32800, 69999]:
+        assert np.array_equal(got[r], reference.adamas_select(Q[r], K[r // rpi], 2, 0, True, 5)), r
