@@ -218,4 +218,75 @@ double output_error(const AttentionOutput& approx, const AttentionOutput& exact)
   return std::sqrt(diff) / std::max(std::sqrt(ref), 1e-30);
 }
 
+// ---------------------------------------------------------------- the sweep harness (f3)
+namespace {
+Dev upload_f64(std::span<const double> x) {
+  Dev d(x.size() * 8);
+  cuda(cudaMemcpy(d.p, x.data(), x.size() * 8, kH2D), "upload f64");
+  return d;
+}
+}  // namespace
+
+CodeStore::CodeStore(std::size_t head_dim, int bits, bool with_hadamard) : head_dim_(head_dim), bits_(bits) {
+  check(adamas_hsel_create(&h_, static_cast<int>(head_dim), bits, with_hadamard ? 1 : 0));
+}
+
+CodeStore::~CodeStore() { adamas_hsel_destroy(h_); }
+
+void CodeStore::build(std::span<const double> keys, std::size_t rows) {
+  if (keys.size() != rows * head_dim_) throw ConfigError("build_cache: keys do not match rows x head_dim");
+  Dev k = upload_f64(keys);
+  check(adamas_hsel_build(h_, static_cast<const double*>(k.p), 1, static_cast<int64_t>(rows), nullptr));
+  rows_ = rows;
+}
+
+SelectionResult CodeStore::select(std::span<const double> query, std::size_t budget, Metric metric) const {
+  if (query.size() != head_dim_) throw ConfigError("score_all: code length differs");
+  SelectionResult r;
+  if (budget == 0) return r;
+  Dev q = upload_f64(query), idx(budget * 8);
+  check(adamas_hsel_select(h_, static_cast<const double*>(q.p), 1, 1,
+                           metric == Metric::manhattan ? ADAMAS_METRIC_MANHATTAN : ADAMAS_METRIC_EUCLIDEAN_SQ,
+                           static_cast<int64_t>(budget), static_cast<int64_t*>(idx.p), nullptr));
+  std::vector<int64_t> h(budget);
+  cuda(cudaMemcpy(h.data(), idx.p, budget * 8, kD2H), "select out");
+  for (int64_t i : h)
+    if (i >= 0) r.indices.push_back(static_cast<std::size_t>(i));
+  return r;
+}
+
+std::vector<std::uint16_t> CodeStore::codes(std::size_t i) const {
+  if (i >= rows_) throw ConfigError("CodeStore: row out of range");
+  const size_t n = bits_ == 3 ? head_dim_ : (head_dim_ + 16 / bits_ - 1) / (16 / bits_);
+  const size_t bytes = bits_ == 3 ? n : n * 2;
+  Dev d(bytes);
+  check(adamas_hsel_codes_ref(h_, static_cast<int64_t>(i), 1, d.p, nullptr));
+  std::vector<std::uint16_t> out(n);
+  if (bits_ == 3) {
+    std::vector<std::uint8_t> b(n);
+    cuda(cudaMemcpy(b.data(), d.p, n, kD2H), "codes");
+    std::copy(b.begin(), b.end(), out.begin());
+  } else {
+    cuda(cudaMemcpy(out.data(), d.p, bytes, kD2H), "codes");
+  }
+  return out;
+}
+
+std::vector<std::size_t> top_k_by_dot(std::span<const double> q, std::span<const double> keys, std::size_t rows,
+                                      std::size_t k) {
+  const size_t d = q.size();
+  if (keys.size() != rows * d) throw ConfigError("top_k_by_dot: keys do not match rows x head_dim");
+  std::vector<std::size_t> r;
+  if (k == 0 || rows == 0) return r;
+  Dev qd = upload_f64(q), kd = upload_f64(keys), idx(k * 8);
+  check(adamas_dot_topk(static_cast<const double*>(qd.p), static_cast<const double*>(kd.p), 1, 1, 1,
+                        static_cast<int64_t>(rows), static_cast<int>(d), static_cast<int64_t>(k),
+                        static_cast<int64_t*>(idx.p), nullptr, nullptr));
+  std::vector<int64_t> h(k);
+  cuda(cudaMemcpy(h.data(), idx.p, k * 8, kD2H), "top_k_by_dot out");
+  for (int64_t i : h)
+    if (i >= 0) r.push_back(static_cast<std::size_t>(i));
+  return r;
+}
+
 }  // namespace adamas::gpu

@@ -115,4 +115,34 @@ DecodeResult decode_step(KvCache& cache, std::span<const double> q, std::span<co
 // attention.cpp:47-57
 double output_error(const AttentionOutput& approx, const AttentionOutput& exact);
 
+// ---------------------------------------------------------------- the sweep harness (f3)
+// The harness's fp64 selection path on the device, any power-of-two head_dim
+// in [2, 1024] and 1/2/3-bit codes: one policy's code store
+// (PolicySpec{adamas, bits, metric, with_hadamard}, sweep.hpp:15-33).
+class CodeStore {
+ public:
+  CodeStore(std::size_t head_dim, int bits = 2, bool with_hadamard = true);
+  ~CodeStore();
+  CodeStore(const CodeStore&) = delete;
+  CodeStore& operator=(const CodeStore&) = delete;
+
+  // build_cache (sweep.cpp:38-50) over `rows` keys (row-major rows x head_dim).
+  void build(std::span<const double> keys, std::size_t rows);
+  // The adamas branch of select (sweep.cpp:87-98): encode, score_all, top_k.
+  SelectionResult select(std::span<const double> query, std::size_t budget, Metric metric = Metric::manhattan) const;
+  // Built codes of row i in the reference's formats: PackedCodes words for
+  // 1/2 bits, CodeVector bytes (one per uint16 here) for 3.
+  std::vector<std::uint16_t> codes(std::size_t i) const;
+  std::size_t rows() const { return rows_; }
+
+ private:
+  adamas_hsel* h_ = nullptr;
+  std::size_t head_dim_, rows_ = 0;
+  int bits_;
+};
+
+// top_k_by_score over dot(q, k_i) (baselines.cpp:21-32): the oracle policy.
+std::vector<std::size_t> top_k_by_dot(std::span<const double> q, std::span<const double> keys, std::size_t rows,
+                                      std::size_t k);
+
 }  // namespace adamas::gpu

@@ -2,6 +2,7 @@
 // C++ facade (adamas::gpu, sm_100a kernels) and checked against the reference's
 // known answers and the C restatement in oracle/ (test infrastructure).
 // Exit code 0 = all passed. Run by tests/test_gpu_facade.py (-m gpu).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
@@ -129,6 +130,56 @@ int main() {
     // degenerate vector -> ConfigError (quantizer.cpp:47)
     std::vector<double> zeros(d, 0.0);
     CHECK(throws_config([&] { encode_pack(zeros, cache); }));
+  }
+  {  // the sweep harness's fp64 selection (f3): codes + select against the C restatement
+    const size_t S = 700;
+    std::vector<double> K;
+    for (size_t i = 0; i < S; ++i) {
+      auto row = synth_vec(5000 + i, d);
+      K.insert(K.end(), row.begin(), row.end());
+    }
+    CodeStore store(d, 2, true);
+    store.build(K, S);
+    bool codes_ok = true;
+    std::vector<uint16_t> ref_words(S * 16);
+    for (size_t i = 0; i < S; ++i) {
+      or_encode_pack(K.data() + i * d, d, ref_words.data() + i * 16);
+      const auto got = store.codes(i);
+      codes_ok &= got.size() == 16 && std::equal(got.begin(), got.end(), ref_words.begin() + i * 16);
+    }
+    CHECK(codes_ok);
+    const auto q = synth_vec(777, d);
+    std::vector<uint16_t> qw(16);
+    or_encode_pack(q.data(), d, qw.data());
+    std::vector<int32_t> sc(S);
+    or_score_all(qw.data(), ref_words.data(), S, 16, sc.data());
+    for (size_t budget : {1u, 64u, 699u, 700u, 900u}) {
+      std::vector<int64_t> ei(budget);
+      const size_t n = or_top_k(sc.data(), S, budget, ei.data());
+      const auto got = store.select(q, budget).indices;
+      bool same = got.size() == n;
+      for (size_t i = 0; i < n && same; ++i) same &= (int64_t)got[i] == ei[i];
+      CHECK(same);
+    }
+    // top_k_by_score over dot products (baselines.cpp:21-32): largest first, ties to the lower index
+    std::vector<double> dots(S);
+    for (size_t i = 0; i < S; ++i) {
+      double acc = 0.0;
+      for (size_t j = 0; j < d; ++j) acc += q[j] * K[i * d + j];
+      dots[i] = acc;
+    }
+    std::vector<size_t> order(S);
+    std::iota(order.begin(), order.end(), size_t{0});
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return dots[a] > dots[b]; });
+    std::vector<size_t> exp(order.begin(), order.begin() + 32);
+    std::sort(exp.begin(), exp.end());
+    CHECK(top_k_by_dot(q, K, S, 32) == exp);
+    CHECK(throws_config([] { CodeStore bad(48, 2, true); }));
+    CHECK(throws_config([] { CodeStore bad(64, 4, true); }));
+    std::vector<double> zk(3 * d, 1.0);
+    std::fill(zk.begin() + d, zk.begin() + 2 * d, 0.0);
+    CodeStore z(d, 2, true);
+    CHECK(throws_config([&] { z.build(zk, 3); }));
   }
   std::printf("facade_tests: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
