@@ -117,9 +117,13 @@ def test_seq_sharded_peer_exchange_two_processes(gpu, tmp_path):
     import sys
     if not torch.cuda.is_available():
         pytest.fail("GPU test selected but no CUDA device is visible")
+    import socket
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:  # a free rendezvous port
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "tests", "p2p_worker.py"),
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "tests", "p2p_worker.py"),
            str(tmp_path)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
