@@ -172,9 +172,27 @@ def cpu_reference(args, n_heads, steps, warmup):
     finally:
         ref.layer_free(layer)
     t = list(t[warmup:])
+    # the reference is single-threaded: also one thread, a shorter sample
+    layer1 = ref.layer_build(n_heads, args.seq - 1, 128, args.dtype == "bf16", 4242, threads)
+    try:
+        t1 = list(ref.layer_decode(layer1, args.budget, 1, 1 + 3)[1:])
+    finally:
+        ref.layer_free(layer1)
     sample = (f"1 layer = {n_heads} heads x S={args.seq} (reference KvCache per head, prebuilt), "
-              f"{len(t)} decode steps, median; simd={ref.simd_level()}")
+              f"{len(t)} decode steps, median, heads over {threads} threads; 1 thread: "
+              f"{statistics.median(t1):.1f} us ({len(t1)} steps); simd={ref.simd_level()}; cpu={_cpu_model()}")
     return float(statistics.median(t)), threads, sample
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -472,7 +490,7 @@ def run_ours(args):
                        "l2": f"no flush: {L * NS} distinct per-(layer, request) caches, "
                              f"{L * NS * n_kv * S * (256 * es + 32) / 2**30:.1f} GiB > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "frac_of_8tbs": achieved / 8000.0,
                          "kernel": "fused_decode_kernel", "bytes_per_launch": bytes_launch,
                          "kernel_us": kern_ms * 1000.0, "peak_source": peak_kind},
             "e2e": {"value": e2e_ms * 1000.0 / (n_e2e * L * tokens_per_layer), "unit": UNIT,
