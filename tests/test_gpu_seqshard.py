@@ -65,6 +65,7 @@ def test_seq_sharded_decode_matches_single_device(gpu, oracle, S, W, n_kv, G, bu
     (5000, 4, 2, 4, 128, True),
     (777, 3, 1, 2, 300, False),
     (64, 4, 1, 1, 128, True),      # empty shards publish empty keys
+    (20000, 8, 2, 4, 128, True),   # the largest world
 ])
 def test_seq_sharded_peer_exchange(gpu, oracle, S, W, n_kv, G, budget, bf16):
     """Peer-memory exchange (mailboxes, epoch flags) instead of all-gathers:
