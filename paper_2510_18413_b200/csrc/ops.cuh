@@ -449,7 +449,10 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   // programmatic dependent launch: keys / the appended row come from the
   // preceding kernel; the next launch may begin its own prologue now
   grid_dependency_wait();
-  if (tid == 0) grid_launch_dependents();
+  // With the fused merge every CTA waits for every other CTA's partial, so all
+  // must be resident: the next launch is not let in early (it could take the
+  // SMs of CTAs not yet placed).
+  if (tid == 0 && merge_out == nullptr) grid_launch_dependents();
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
   if (tid == 0) {
     n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0;
