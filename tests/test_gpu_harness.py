@@ -264,3 +264,41 @@ def test_select_many_rows_chunked(gpu, reference):
     got = sel.select(torch.as_tensor(Q, device="cuda"), 5, "l1", rows_per_inst=rpi).cpu().numpy()
     for r in [0, 1, 32767, 32768, 32800, 69999]:
         assert np.array_equal(got[r], reference.adamas_select(Q[r], K[r // rpi], 2, 0, True, 5)), r
+
+
+def test_acceptance_ablation_criterion(gpu, reference):
+    """acceptance.cpp:346-413 (all 120 seeds) with every selection on the GPU:
+    the Hadamard transform helps significantly, 3 >= 2 >= 1 bits up to noise,
+    diminishing returns from 2 to 3 bits; rows equal the reference's."""
+    seeds, z95, budgets = 120, 1.645, [16, 64, 256]
+    sweep = H.SweepConfig(budgets=budgets, policies=[H.PolicySpec("adamas", bits=2),
+                                                     H.PolicySpec("adamas", bits=2, with_hadamard=False),
+                                                     H.PolicySpec("adamas", bits=1), H.PolicySpec("adamas", bits=3)],
+                          measure_output_error=False)
+    specs = [H.WorkloadSpec(seed=9000 + s, seq_len=2048, head_dim=128, num_queries=1,
+                            distribution="gaussian_with_outliers", outlier_frac=0.01, outlier_scale=10.0)
+             for s in range(seeds)]
+    insts = [ref_instances(reference, sp)[0] for sp in specs]
+    rows = H.run_sweep(insts, sweep)  # one batched sweep: instance s = seed s
+    n_cells = len(sweep.policies) * len(budgets)
+    assert len(rows) == n_cells * seeds
+    rec = np.array([r.recall for r in rows]).reshape(len(sweep.policies), len(budgets), seeds)
+    for s in range(3):  # per-seed rows equal the reference's own sweep
+        csv, _, _ = reference.run_sweep(specs[s], sweep)
+        mine = [rows[c * seeds + s] for c in range(n_cells)]
+        assert H.rows_to_csv(mine) == csv
+
+    def paired(a, b):
+        d = a - b
+        return d.mean(), np.sqrt(d.var(ddof=1) / d.size)
+
+    for bi in range(len(budgets)):
+        with2, without2, with1, with3 = rec[0, bi], rec[1, bi], rec[2, bi], rec[3, bi]
+        m, se = paired(with2, without2)
+        assert m > z95 * se, ("transform gain not significant", budgets[bi], m, se)
+        m, se = paired(with3, with2)
+        assert m > -z95 * se, ("3-bit below 2-bit", budgets[bi])
+        m, se = paired(with2, with1)
+        assert m > -z95 * se, ("2-bit below 1-bit", budgets[bi])
+        m, se = paired((with3 - with2) - (with2 - with1), np.zeros(seeds))
+        assert m < z95 * se, ("no diminishing returns", budgets[bi], m)
