@@ -165,6 +165,12 @@ def test_attention_f64(gpu, reference):
     full = H.attention_f64(Qd, Kd, Vd, rows_per_inst=nq).cpu().numpy()
     idx = torch.as_tensor(np.tile(np.arange(0, S, 3), (nq, 1)), device="cuda")
     part = H.attention_f64(Qd, Kd, Vd, nq, idx).cpu().numpy()
+    # acceptance.cpp:155-205: sparse over the full set == dense (here bit for
+    # bit: same kernel, same order), a singleton selection returns its value row
+    every = torch.as_tensor(np.tile(np.arange(S), (nq, 1)), device="cuda")
+    assert np.array_equal(H.attention_f64(Qd, Kd, Vd, nq, every).cpu().numpy(), full)
+    one = torch.as_tensor(np.array([[5], [77], [699]]), device="cuda")
+    assert np.array_equal(H.attention_f64(Qd, Kd, Vd, nq, one).cpu().numpy(), V[[5, 77, 699]])
     for r in range(nq):
         e = reference.full_attention(Q[r], K, V)
         assert np.abs(full[r] - e).max() <= 1e-12 * np.abs(e).max()
