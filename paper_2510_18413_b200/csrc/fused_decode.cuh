@@ -34,6 +34,12 @@
 
 namespace adamas_dev {
 
+#ifndef ADAMAS_SPAN_MASKS
+#define ADAMAS_SPAN_MASKS 1  // compaction: register span masks with rotated reads (1) or 32-token groups (0)
+#endif
+#ifndef ADAMAS_GATHER_PREFETCH
+#define ADAMAS_GATHER_PREFETCH 1  // L2-prefetch the rows at distance <= T in the count pass
+#endif
 #ifndef ADAMAS_CWARPS
 #define ADAMAS_CWARPS 16  // consumer warps per CTA: 16 (1 CTA/SM) or 8 (2 CTAs/SM)
 #endif
@@ -226,6 +232,23 @@ __device__ __forceinline__ void group_masks(const uint16_t* d32, int thr, int va
   const uint32_t vm = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
   ltm = lt & vm;
   eqm = (le & ~lt) & vm;
+}
+
+// 8-token masks (bit e = token e of a 16-B chunk of u16 distances) of
+// distances <= thr and < thr, same SWAR as group_masks.
+__device__ __forceinline__ void chunk_masks(const uint4 v4, int thr, uint32_t& le, uint32_t& lt) {
+  const uint32_t kle = ((uint32_t)thr * 0x00010001u) | 0x80008000u;
+  const uint32_t klt = thr > 0 ? (((uint32_t)(thr - 1) * 0x00010001u) | 0x80008000u) : 0u;
+  const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+  le = 0u;
+  lt = 0u;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t a = (kle - w[e]) & 0x80008000u;
+    const uint32_t b = thr > 0 ? ((klt - w[e]) & 0x80008000u) : 0u;
+    le |= ((a >> 15) & 1u) << (2 * e) | (a >> 31) << (2 * e + 1);
+    lt |= ((b >> 15) & 1u) << (2 * e) | (b >> 31) << (2 * e + 1);
+  }
 }
 
 template <typename T, int G>
@@ -577,8 +600,13 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   ADAMAS_TRACE(5);
 
   // ---------------------------------------------------------------- compaction
-  // Thread t_in of head g owns a contiguous run of 32-token groups: count
-  // (< T, == T) -> head-segmented prefix in index order -> emit.
+  // Thread t_in of head g owns a contiguous span of tokens: count (< T, == T)
+  // -> head-segmented prefix in index order -> emit. Spans of 16, 32 or 64
+  // tokens (the smallest that covers the rank with the head's NT threads) keep
+  // their masks in registers between the two passes, and read the distances
+  // in a rotated 16-B chunk order so the 8 threads of a shared-memory wavefront
+  // hit 8 distinct bank groups; longer ranks take 32-token groups per thread
+  // and recompute the masks.
   {
     const int g = g_me;
     const int ngroups = (len + 31) >> 5;
@@ -591,23 +619,64 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     const uint16_t* dg = dist + g * p.chunk;
     const T* Kg = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
     const T* Vg = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
-    int my_lt = 0, my_eq = 0;
-    for (int grp = grp0; grp < grp1; ++grp) {
-      uint32_t ltm, eqm;
-      group_masks(dg + grp * 32, thr, len - grp * 32, ltm, eqm);
-      my_lt += __popc(ltm);
-      my_eq += __popc(eqm);
-      // warm L2 for the gather: every row at distance <= T (a superset of the
-      // survivors), one prefetch per 128-B line
-      for (uint32_t m = ltm | eqm; m; m &= m - 1) {
-        const int t = grp * 32 + __ffs(m) - 1;
-        const char* kp = reinterpret_cast<const char*>(Kg + (int64_t)t * kHeadDim);
-        const char* vp = reinterpret_cast<const char*>(Vg + (int64_t)t * kHeadDim);
+    int sh = 0;
+    while (sh < 2 && (NT << (4 + sh)) < ngroups * 32) ++sh;
+    const bool span = ADAMAS_SPAN_MASKS && (NT << (4 + sh)) >= ngroups * 32;  // CTA-uniform
+    const int tok0 = t_in << (4 + sh);
+    uint32_t sl[2] = {0u, 0u}, se[2] = {0u, 0u};  // span masks: bit i of word w = token tok0 + 32 w + i
+    // warm L2 for the gather: every row at distance <= T (a superset of the
+    // survivors), one prefetch per 128-B line
+    auto prefetch_row = [&](int t) {
+      const char* kp = reinterpret_cast<const char*>(Kg + (int64_t)t * kHeadDim);
+      const char* vp = reinterpret_cast<const char*>(Vg + (int64_t)t * kHeadDim);
 #pragma unroll
-        for (int c = 0; c < (int)(kHeadDim * sizeof(T)); c += 128) {
-          prefetch_l2(kp + c);
-          prefetch_l2(vp + c);
+      for (int c = 0; c < (int)(kHeadDim * sizeof(T)); c += 128) {
+        prefetch_l2(kp + c);
+        prefetch_l2(vp + c);
+      }
+    };
+    int my_lt = 0, my_eq = 0;
+    if (span) {
+      if (tok0 < len) {
+        const int nch = 2 << sh;             // 16-B chunks (8 tokens) per span
+        const int rot = (t_in * nch) >> 3;   // chunk rotation: distinct bank groups per wavefront
+        const uint4* src = reinterpret_cast<const uint4*>(dg + tok0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < nch) {
+            const int c = (j + rot) & (nch - 1);
+            uint32_t le8, lt8;
+            chunk_masks(src[c], thr, le8, lt8);
+            const int sft = (c & 3) * 8;
+            if (c < 4) {
+              sl[0] |= lt8 << sft;
+              se[0] |= (le8 & ~lt8) << sft;
+            } else {
+              sl[1] |= lt8 << sft;
+              se[1] |= (le8 & ~lt8) << sft;
+            }
+          }
         }
+        const int v = len - tok0;  // valid tokens in the span (>= 1)
+        const uint32_t vm0 = v >= 32 ? 0xffffffffu : (1u << v) - 1u;
+        const uint32_t vm1 = v >= 64 ? 0xffffffffu : (v <= 32 ? 0u : (1u << (v - 32)) - 1u);
+        sl[0] &= vm0; se[0] &= vm0;
+        sl[1] &= vm1; se[1] &= vm1;
+      }
+      my_lt = __popc(sl[0]) + __popc(sl[1]);
+      my_eq = __popc(se[0]) + __popc(se[1]);
+#pragma unroll
+      for (int w = 0; w < 2; ++w)
+        for (uint32_t m = ADAMAS_GATHER_PREFETCH ? (sl[w] | se[w]) : 0u; m; m &= m - 1)
+          prefetch_row(tok0 + 32 * w + __ffs(m) - 1);
+    } else {
+      for (int grp = grp0; grp < grp1; ++grp) {
+        uint32_t ltm, eqm;
+        group_masks(dg + grp * 32, thr, len - grp * 32, ltm, eqm);
+        my_lt += __popc(ltm);
+        my_eq += __popc(eqm);
+        for (uint32_t m = ADAMAS_GATHER_PREFETCH ? (ltm | eqm) : 0u; m; m &= m - 1)
+          prefetch_row(grp * 32 + __ffs(m) - 1);
       }
     }
     int lt_before, eq_before, lt_tot, eq_tot;
@@ -620,27 +689,39 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
                              : nullptr;
       int pos = lt_before + min(eq_before, eq_budget);
       int eq_seen = eq_before;
-      for (int grp = grp0; grp < grp1; ++grp) {
-        uint32_t ltm, eqm;
-        group_masks(dg + grp * 32, thr, len - grp * 32, ltm, eqm);
-        for (uint32_t m = ltm | eqm; m; m &= m - 1) {
-          const int i = __ffs(m) - 1;
-          if ((eqm >> i) & 1u) {
-            if (eq_seen++ >= eq_budget) continue;  // ties beyond the budget are not taken
+      // local token t (in index order) at distance <= T: take it unless it is
+      // a tie beyond the budget
+      auto emit = [&](int t, bool is_eq) {
+        if (is_eq && eq_seen++ >= eq_budget) return;  // ties beyond the budget are not taken
+        const int tok = (int)start + t;
+        if (pos < selcap) sel[g * selcap + pos] = tok;
+        if (idx_row) idx_row[pos] = tok;
+        if (p.cand) {  // (distance, global index) key: the distributed top-k's order
+          const int64_t off = ((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos;
+          const uint32_t key = ((uint32_t)dg[t] << 23) | (uint32_t)(p.cand_base + tok);
+          if (p.peers.n) {
+            for (int r = 0; r < p.peers.n; ++r) p.peers.keys[r][off] = key;  // NVLink stores
+          } else {
+            p.cand[off] = key;
           }
-          const int tok = (int)start + grp * 32 + i;
-          if (pos < selcap) sel[g * selcap + pos] = tok;
-          if (idx_row) idx_row[pos] = tok;
-          if (p.cand) {  // (distance, global index) key: the distributed top-k's order
-            const int64_t off = ((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos;
-            const uint32_t key = ((uint32_t)dg[grp * 32 + i] << 23) | (uint32_t)(p.cand_base + tok);
-            if (p.peers.n) {
-              for (int r = 0; r < p.peers.n; ++r) p.peers.keys[r][off] = key;  // NVLink stores
-            } else {
-              p.cand[off] = key;
-            }
+        }
+        ++pos;
+      };
+      if (span) {
+#pragma unroll
+        for (int w = 0; w < 2; ++w)
+          for (uint32_t m = sl[w] | se[w]; m; m &= m - 1) {
+            const int i = __ffs(m) - 1;
+            emit(tok0 + 32 * w + i, (se[w] >> i) & 1u);
           }
-          ++pos;
+      } else {
+        for (int grp = grp0; grp < grp1; ++grp) {
+          uint32_t ltm, eqm;
+          group_masks(dg + grp * 32, thr, len - grp * 32, ltm, eqm);
+          for (uint32_t m = ltm | eqm; m; m &= m - 1) {
+            const int i = __ffs(m) - 1;
+            emit(grp * 32 + i, (eqm >> i) & 1u);
+          }
         }
       }
     }
