@@ -184,6 +184,31 @@ def test_fused_decode_exchange_topologies(gpu, oracle, monkeypatch, cluster, G):
     run_decode(gpu, oracle, 5000, 1, G, 96, True, seed=31 * G + int(cluster), steps=2)
 
 
+@pytest.mark.parametrize("S,G", [(8000, 1), (16000, 1), (32000, 1), (40000, 1),
+                                 (2000, 4), (4000, 4), (8000, 4), (9000, 4)])
+def test_fused_compaction_span_sizes(gpu, oracle, monkeypatch, S, G):
+    """one CTA per unit, so the rank length picks the compaction form: register
+    masks over 16 / 32 / 64-token spans per thread, or 32-token groups beyond"""
+    monkeypatch.setenv("ADAMAS_CLUSTER", "1")
+    run_decode(gpu, oracle, S, 1, G, 128, True, seed=S + 13 * G, steps=2)
+
+
+@pytest.mark.parametrize("cluster", ["1", "4"])
+def test_fused_decode_heavy_ties(gpu, oracle, monkeypatch, cluster):
+    """keys drawn from 6 distinct vectors: whole bins of equal distances at T,
+    ties taken in index order across spans and ranks (estimator.cpp:75-90)"""
+    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    S, n_kv, G, budget = 6001, 1, 2, 100
+    K, V, q = make_inputs(S, n_kv, n_kv * G, True, 4242)
+    pick = np.random.default_rng(7).integers(0, 6, S)
+    K = K[:6][pick]
+    cache = fill_cache(gpu, K[:-1], V[:-1], True, capacity=S + 4)
+    out, idx = cache.decode_step(to_dev(q, True), to_dev(K[-1], True), to_dev(V[-1], True), budget)
+    _, _, eidx, eout = oracle_decode(oracle, K, V, q, budget)
+    assert np.array_equal(idx.cpu().numpy(), eidx)
+    assert rel_err(out.cpu().numpy(), eout).max() <= TOL[True]
+
+
 def test_operator_composition_matches_fused(gpu, oracle, monkeypatch):
     monkeypatch.setenv("ADAMAS_NO_FUSED", "1")
     run_decode(gpu, oracle, 2000, 2, 2, 64, False, seed=5, steps=2)
