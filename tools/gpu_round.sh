@@ -14,3 +14,6 @@ timeout 300 python tools/prefill_bench.py > gpurun_out/prefill.json 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --layers 4 --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_decode -s 8 -c 1 -o gpurun_out/prof_fused python bench.py --steps 2 --warmup 3 --layers 4 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
+# config 2 (Llama GQA 128K): the q-split scan's L2 traffic
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_decode -s 4 -c 1 -o gpurun_out/prof_llama python bench.py --config llama128k --steps 2 --warmup 3 --layers 2 --no-cpu-baseline > gpurun_out/ncu_llama.log 2>&1
+ls -la gpurun_out

@@ -56,6 +56,11 @@ WANT = [
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__grid_size", "launch__block_size", "launch__cluster_size", "launch__registers_per_thread",
     "launch__shared_mem_per_block_dynamic", "sm__cycles_active.avg", "gpc__cycles_elapsed.max",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "lts__t_sectors_op_read.sum", "lts__t_bytes.sum",
 ]
 
 
