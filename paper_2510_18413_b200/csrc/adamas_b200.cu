@@ -160,9 +160,9 @@ int ensure_unit_scratch(adamas_cache* c, size_t slots) {
 }
 
 // ----------------------------------------------------------------- fused launcher
-template <typename T, int G>
+template <typename T, int G, int SW>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
-  auto kern = fused_decode_kernel<T, G>;
+  auto kern = fused_decode_kernel<T, G, SW>;
   static bool configured = false;
   static size_t configured_smem = 0;
   if (!configured || configured_smem < smem) {
@@ -213,11 +213,14 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
 
 template <typename T>
 int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaStream_t s) {
+  // 4-word compaction spans only where a rank needs 64..128 tokens per thread
+  const int nt = kConsumers / G;
+  const bool wide = (int64_t)prm.chunk > (int64_t)nt * 64 && (int64_t)prm.chunk <= (int64_t)nt * 128;
   switch (G) {
-    case 1: return launch_fused_t<T, 1>(prm, C, smem, s);
-    case 2: return launch_fused_t<T, 2>(prm, C, smem, s);
-    case 4: return launch_fused_t<T, 4>(prm, C, smem, s);
-    case 8: return launch_fused_t<T, 8>(prm, C, smem, s);
+    case 1: return wide ? launch_fused_t<T, 1, 4>(prm, C, smem, s) : launch_fused_t<T, 1, 2>(prm, C, smem, s);
+    case 2: return wide ? launch_fused_t<T, 2, 4>(prm, C, smem, s) : launch_fused_t<T, 2, 2>(prm, C, smem, s);
+    case 4: return wide ? launch_fused_t<T, 4, 4>(prm, C, smem, s) : launch_fused_t<T, 4, 2>(prm, C, smem, s);
+    case 8: return wide ? launch_fused_t<T, 8, 4>(prm, C, smem, s) : launch_fused_t<T, 8, 2>(prm, C, smem, s);
   }
   return kFusedUnsupported;
 }

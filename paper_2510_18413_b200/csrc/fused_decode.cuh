@@ -35,7 +35,7 @@
 namespace adamas_dev {
 
 #ifndef ADAMAS_SPAN_MASKS
-#define ADAMAS_SPAN_MASKS 1  // compaction: register span masks with rotated reads (1) or 32-token groups (0)
+#define ADAMAS_SPAN_MASKS 1  // compaction: register span masks over a swizzled layout (1) or 32-token groups (0)
 #endif
 #ifndef ADAMAS_GATHER_PREFETCH
 #define ADAMAS_GATHER_PREFETCH 1  // L2-prefetch the rows at distance <= T in the count pass
@@ -251,7 +251,9 @@ __device__ __forceinline__ void chunk_masks(const uint4 v4, int thr, uint32_t& l
   }
 }
 
-template <typename T, int G>
+// SW: mask words of the longest compaction span (32 tokens each): 2, or 4
+// for ranks of 64..128 tokens per thread (more registers, so only then).
+template <typename T, int G, int SW>
 __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   static_assert(G >= 1 && G <= kMaxG && (kConsumerWarps % G) == 0, "G must divide the warp count");
   constexpr int WG = kConsumerWarps / G;  // consumer warps per q-head
@@ -418,6 +420,25 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 #pragma unroll
   for (int g = 0; g < G; ++g) qc[g] = make_qcode(qcode[g]);
 
+  // Compaction geometry, fixed before the scan because it sets the distance
+  // layout: thread t of a head owns a span of 16 << sh tokens (the smallest
+  // that covers the rank with the head's NT threads, up to 128), and the
+  // 16-B chunks of span s are stored XOR-swizzled by swz(s), so the 8 threads
+  // of a shared-memory wavefront reading chunk j of their spans hit 8
+  // distinct bank groups. Longer ranks keep the plain layout (32-token groups).
+  const int span_groups = (len + 31) >> 5;
+  int sh = 0;
+  while ((2 << sh) < 4 * SW && (NT << (4 + sh)) < span_groups * 32) ++sh;
+  const bool span = ADAMAS_SPAN_MASKS && (NT << (4 + sh)) >= span_groups * 32;  // CTA-uniform
+  const int nch = 2 << sh;  // 16-B chunks (8 tokens) per span
+  auto swz = [&](int sp) { return nch >= 8 ? (sp & 7) : ((sp * nch) >> 3) & (nch - 1); };
+  // shared-memory slot of local token x in a head's distance row; for
+  // x = base + j (base a multiple of 1024) it is base + dslot(j)
+  auto dslot = [&](int x) { return span ? x ^ (swz(x >> (4 + sh)) << 3) : x; };
+  int jslot[kTokPerThread];
+#pragma unroll
+  for (int u = 0; u < kTokPerThread; ++u) jslot[u] = dslot(tid + u * kConsumers);
+
   // ---------------------------------------------------------------- scan
   ADAMAS_TRACE(2);
   for (int st = 0; st < n_stages; ++st) {
@@ -448,7 +469,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       if (j < ntok) {
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          dist[g * p.chunk + base + j] = (uint16_t)d[u][g];
+          dist[g * p.chunk + base + jslot[u]] = (uint16_t)d[u][g];
           atomicAdd(&hist[g * kHistBins + d[u][g]], 1);
         }
       }
@@ -460,7 +481,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 #pragma unroll
     for (int w = 0; w < 4; ++w) nx[w] = nc.lo[w] ^ nc.hi[w];
     const uint32_t d = l1_distance(make_qcode(qcode[tid]), nc.lo, nx);
-    dist[tid * p.chunk + (int)(s_old - start)] = (uint16_t)d;
+    dist[tid * p.chunk + dslot((int)(s_old - start))] = (uint16_t)d;
     atomicAdd(&hist[tid * kHistBins + d], 1);
   }
   consumer_sync();  // local histogram final
@@ -601,12 +622,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 
   // ---------------------------------------------------------------- compaction
   // Thread t_in of head g owns a contiguous span of tokens: count (< T, == T)
-  // -> head-segmented prefix in index order -> emit. Spans of 16, 32 or 64
-  // tokens (the smallest that covers the rank with the head's NT threads) keep
-  // their masks in registers between the two passes, and read the distances
-  // in a rotated 16-B chunk order so the 8 threads of a shared-memory wavefront
-  // hit 8 distinct bank groups; longer ranks take 32-token groups per thread
-  // and recompute the masks.
+  // -> head-segmented prefix in index order -> emit. Spans (16..128 tokens,
+  // swizzled distance layout, see before the scan) keep their masks in
+  // registers between the two passes; longer ranks take 32-token groups per
+  // thread and recompute the masks.
   {
     const int g = g_me;
     const int ngroups = (len + 31) >> 5;
@@ -619,11 +638,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     const uint16_t* dg = dist + g * p.chunk;
     const T* Kg = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
     const T* Vg = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
-    int sh = 0;
-    while (sh < 2 && (NT << (4 + sh)) < ngroups * 32) ++sh;
-    const bool span = ADAMAS_SPAN_MASKS && (NT << (4 + sh)) >= ngroups * 32;  // CTA-uniform
     const int tok0 = t_in << (4 + sh);
-    uint32_t sl[2] = {0u, 0u}, se[2] = {0u, 0u};  // span masks: bit i of word w = token tok0 + 32 w + i
+    uint32_t sl[SW], se[SW];  // span masks: bit i of word w = token tok0 + 32 w + i
+#pragma unroll
+    for (int w = 0; w < SW; ++w) sl[w] = se[w] = 0u;
     // warm L2 for the gather: every row at distance <= T (a superset of the
     // survivors), one prefetch per 128-B line
     auto prefetch_row = [&](int t) {
@@ -638,35 +656,33 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     int my_lt = 0, my_eq = 0;
     if (span) {
       if (tok0 < len) {
-        const int nch = 2 << sh;             // 16-B chunks (8 tokens) per span
-        const int rot = (t_in * nch) >> 3;   // chunk rotation: distinct bank groups per wavefront
+        const int z = swz(t_in);  // this span's chunk swizzle
         const uint4* src = reinterpret_cast<const uint4*>(dg + tok0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4 * SW; ++j) {
           if (j < nch) {
-            const int c = (j + rot) & (nch - 1);
             uint32_t le8, lt8;
-            chunk_masks(src[c], thr, le8, lt8);
-            const int sft = (c & 3) * 8;
-            if (c < 4) {
-              sl[0] |= lt8 << sft;
-              se[0] |= (le8 & ~lt8) << sft;
-            } else {
-              sl[1] |= lt8 << sft;
-              se[1] |= (le8 & ~lt8) << sft;
-            }
+            chunk_masks(src[j ^ z], thr, le8, lt8);
+            sl[j >> 2] |= lt8 << ((j & 3) * 8);
+            se[j >> 2] |= (le8 & ~lt8) << ((j & 3) * 8);
           }
         }
         const int v = len - tok0;  // valid tokens in the span (>= 1)
-        const uint32_t vm0 = v >= 32 ? 0xffffffffu : (1u << v) - 1u;
-        const uint32_t vm1 = v >= 64 ? 0xffffffffu : (v <= 32 ? 0u : (1u << (v - 32)) - 1u);
-        sl[0] &= vm0; se[0] &= vm0;
-        sl[1] &= vm1; se[1] &= vm1;
-      }
-      my_lt = __popc(sl[0]) + __popc(sl[1]);
-      my_eq = __popc(se[0]) + __popc(se[1]);
 #pragma unroll
-      for (int w = 0; w < 2; ++w)
+        for (int w = 0; w < SW; ++w) {
+          const int vw = v - 32 * w;
+          const uint32_t vm = vw >= 32 ? 0xffffffffu : (vw <= 0 ? 0u : (1u << vw) - 1u);
+          sl[w] &= vm;
+          se[w] &= vm;
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < SW; ++w) {
+        my_lt += __popc(sl[w]);
+        my_eq += __popc(se[w]);
+      }
+#pragma unroll
+      for (int w = 0; w < SW; ++w)
         for (uint32_t m = ADAMAS_GATHER_PREFETCH ? (sl[w] | se[w]) : 0u; m; m &= m - 1)
           prefetch_row(tok0 + 32 * w + __ffs(m) - 1);
     } else {
@@ -698,7 +714,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         if (idx_row) idx_row[pos] = tok;
         if (p.cand) {  // (distance, global index) key: the distributed top-k's order
           const int64_t off = ((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos;
-          const uint32_t key = ((uint32_t)dg[t] << 23) | (uint32_t)(p.cand_base + tok);
+          const uint32_t key = ((uint32_t)dg[dslot(t)] << 23) | (uint32_t)(p.cand_base + tok);
           if (p.peers.n) {
             for (int r = 0; r < p.peers.n; ++r) p.peers.keys[r][off] = key;  // NVLink stores
           } else {
@@ -709,7 +725,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       };
       if (span) {
 #pragma unroll
-        for (int w = 0; w < 2; ++w)
+        for (int w = 0; w < SW; ++w)
           for (uint32_t m = sl[w] | se[w]; m; m &= m - 1) {
             const int i = __ffs(m) - 1;
             emit(tok0 + 32 * w + i, (se[w] >> i) & 1u);

@@ -25,6 +25,7 @@ ap.add_argument("--budget", type=int, default=128)
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--cluster", default="")
 ap.add_argument("--traced", type=int, default=-1, help="index of the traced layer")
+ap.add_argument("--seqs", type=int, default=1, help="independent sequences per launch (batched decode)")
 args = ap.parse_args()
 if args.cluster:
     os.environ["ADAMAS_CLUSTER"] = args.cluster
@@ -33,16 +34,19 @@ from paper_2510_18413_b200._lib import load  # noqa: E402
 
 L = load()
 gen = torch.Generator(device="cuda").manual_seed(0)
-caches = []
+caches = []  # [layer][sequence]
 for _ in range(args.layers):
-    c = ad.KvCache(args.kv_heads, args.seq + 1, torch.bfloat16)
-    for s0 in range(0, args.seq - 1, 4096):
-        n = min(4096, args.seq - 1 - s0)
-        c.update(torch.randn((n, args.kv_heads, 128), generator=gen, device="cuda").bfloat16(),
-                 torch.randn((n, args.kv_heads, 128), generator=gen, device="cuda").bfloat16())
-    caches.append(c)
-q = torch.randn((args.heads, 128), generator=gen, device="cuda").bfloat16()
-k = torch.randn((args.kv_heads, 128), generator=gen, device="cuda").bfloat16()
+    per = []
+    for _ in range(args.seqs):
+        c = ad.KvCache(args.kv_heads, args.seq + 1, torch.bfloat16)
+        for s0 in range(0, args.seq - 1, 4096):
+            n = min(4096, args.seq - 1 - s0)
+            c.update(torch.randn((n, args.kv_heads, 128), generator=gen, device="cuda").bfloat16(),
+                     torch.randn((n, args.kv_heads, 128), generator=gen, device="cuda").bfloat16())
+        per.append(c)
+    caches.append(per)
+q = torch.randn((args.seqs, args.heads, 128), generator=gen, device="cuda").bfloat16()
+k = torch.randn((args.seqs, args.kv_heads, 128), generator=gen, device="cuda").bfloat16()
 trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
 names = ["start", "prologue (zero, q load, barrier init)", "encode + append", "scan", "hist exchange",
          "threshold", "compact count (+L2 prefetch) + scan", "compact emit",
@@ -51,10 +55,15 @@ base_dbg = int(os.environ.get("ADAMAS_DBG", "0")) & 0xff
 
 
 def run_layers():
-    for c in caches:
-        L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if c is caches[args.traced] else None)
-        c.decode_step(q, k, k, args.budget)
-        c.truncate(args.seq - 1)
+    for li, per in enumerate(caches):
+        traced = li == (args.traced % len(caches))
+        L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if traced else None)
+        if args.seqs == 1:
+            per[0].decode_step(q[0], k[0], k[0], args.budget)
+        else:
+            ad.decode_step_batched(per, q, k, k, args.budget)
+        for c in per:
+            c.truncate(args.seq - 1)
     L.adamas_debug_trace(None)
 
 
