@@ -38,7 +38,7 @@ namespace adamas_dev {
 #define ADAMAS_SPAN_MASKS 1  // compaction: register span masks over a swizzled layout (1) or 32-token groups (0)
 #endif
 #ifndef ADAMAS_GATHER_PREFETCH
-#define ADAMAS_GATHER_PREFETCH 1  // L2-prefetch the rows at distance <= T in the count pass
+#define ADAMAS_GATHER_PREFETCH 2  // L2-prefetch the gather rows: 1 all rows <= T in the count pass, 2 survivors in the emit, 0 none
 #endif
 #ifndef ADAMAS_CWARPS
 #define ADAMAS_CWARPS 16  // consumer warps per CTA: 16 (1 CTA/SM) or 8 (2 CTAs/SM)
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       }
 #pragma unroll
       for (int w = 0; w < SW; ++w)
-        for (uint32_t m = ADAMAS_GATHER_PREFETCH ? (sl[w] | se[w]) : 0u; m; m &= m - 1)
+        for (uint32_t m = ADAMAS_GATHER_PREFETCH == 1 ? (sl[w] | se[w]) : 0u; m; m &= m - 1)
           prefetch_row(tok0 + 32 * w + __ffs(m) - 1);
     } else {
       for (int grp = grp0; grp < grp1; ++grp) {
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         group_masks(dg + grp * 32, thr, len - grp * 32, ltm, eqm);
         my_lt += __popc(ltm);
         my_eq += __popc(eqm);
-        for (uint32_t m = ADAMAS_GATHER_PREFETCH ? (ltm | eqm) : 0u; m; m &= m - 1)
+        for (uint32_t m = ADAMAS_GATHER_PREFETCH == 1 ? (ltm | eqm) : 0u; m; m &= m - 1)
           prefetch_row(grp * 32 + __ffs(m) - 1);
       }
     }
@@ -710,6 +710,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       auto emit = [&](int t, bool is_eq) {
         if (is_eq && eq_seen++ >= eq_budget) return;  // ties beyond the budget are not taken
         const int tok = (int)start + t;
+        if (ADAMAS_GATHER_PREFETCH == 2 && !p.cand) prefetch_row(t);
         if (pos < selcap) sel[g * selcap + pos] = tok;
         if (idx_row) idx_row[pos] = tok;
         if (p.cand) {  // (distance, global index) key: the distributed top-k's order
