@@ -642,8 +642,9 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     uint32_t sl[SW], se[SW];  // span masks: bit i of word w = token tok0 + 32 w + i
 #pragma unroll
     for (int w = 0; w < SW; ++w) sl[w] = se[w] = 0u;
-    // warm L2 for the gather: every row at distance <= T (a superset of the
-    // survivors), one prefetch per 128-B line
+    // warm L2 for the gather, one prefetch per 128-B line: each survivor as
+    // the emit places it (default), or every row at distance <= T in the
+    // count pass (ADAMAS_GATHER_PREFETCH = 1)
     auto prefetch_row = [&](int t) {
       const char* kp = reinterpret_cast<const char*>(Kg + (int64_t)t * kHeadDim);
       const char* vp = reinterpret_cast<const char*>(Vg + (int64_t)t * kHeadDim);
