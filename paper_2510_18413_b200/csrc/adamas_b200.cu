@@ -160,9 +160,9 @@ int ensure_unit_scratch(adamas_cache* c, size_t slots) {
 }
 
 // ----------------------------------------------------------------- fused launcher
-template <typename T, int G, int SW>
+template <typename T, int G, int SW, bool FULL>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
-  auto kern = fused_decode_kernel<T, G, SW>;
+  auto kern = fused_decode_kernel<T, G, SW, FULL>;
   static bool configured = false;
   static size_t configured_smem = 0;
   if (!configured || configured_smem < smem) {
@@ -216,11 +216,22 @@ int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaSt
   // 4-word compaction spans only where a rank needs 64..128 tokens per thread
   const int nt = kConsumers / G;
   const bool wide = (int64_t)prm.chunk > (int64_t)nt * 64 && (int64_t)prm.chunk <= (int64_t)nt * 128;
+  // the full instance (two-hop exchange, multi-cluster units, candidates)
+  // only where the launch needs it
+  const bool full = prm.P > 1 || prm.cand != nullptr || C * G > 8;
   switch (G) {
-    case 1: return wide ? launch_fused_t<T, 1, 4>(prm, C, smem, s) : launch_fused_t<T, 1, 2>(prm, C, smem, s);
-    case 2: return wide ? launch_fused_t<T, 2, 4>(prm, C, smem, s) : launch_fused_t<T, 2, 2>(prm, C, smem, s);
-    case 4: return wide ? launch_fused_t<T, 4, 4>(prm, C, smem, s) : launch_fused_t<T, 4, 2>(prm, C, smem, s);
-    case 8: return wide ? launch_fused_t<T, 8, 4>(prm, C, smem, s) : launch_fused_t<T, 8, 2>(prm, C, smem, s);
+    case 1:
+      return full ? launch_fused_t<T, 1, 2, true>(prm, C, smem, s)
+                  : wide ? launch_fused_t<T, 1, 4, false>(prm, C, smem, s) : launch_fused_t<T, 1, 2, false>(prm, C, smem, s);
+    case 2:
+      return full ? launch_fused_t<T, 2, 2, true>(prm, C, smem, s)
+                  : wide ? launch_fused_t<T, 2, 4, false>(prm, C, smem, s) : launch_fused_t<T, 2, 2, false>(prm, C, smem, s);
+    case 4:
+      return full ? launch_fused_t<T, 4, 2, true>(prm, C, smem, s)
+                  : wide ? launch_fused_t<T, 4, 4, false>(prm, C, smem, s) : launch_fused_t<T, 4, 2, false>(prm, C, smem, s);
+    case 8:
+      return full ? launch_fused_t<T, 8, 2, true>(prm, C, smem, s)
+                  : wide ? launch_fused_t<T, 8, 4, false>(prm, C, smem, s) : launch_fused_t<T, 8, 2, false>(prm, C, smem, s);
   }
   return kFusedUnsupported;
 }

@@ -251,9 +251,30 @@ __device__ __forceinline__ void chunk_masks(const uint4 v4, int thr, uint32_t& l
   }
 }
 
+// encode128 (certified fp32, exact fp64 fallback) with the code stored to
+// *dst by lane 0; exact = true forces the fp64 path. (The fallback stays
+// inline: as a noinline call it cost 0.45 µs per layer at config 1.)
+__device__ __forceinline__ bool encode128_to(const float in[4], double* sq, Code* dst, bool exact) {
+  Code c;
+  if (!exact) {
+    const int r = encode128_warp_f32(in, c);
+    if (r == 1) {
+      if ((threadIdx.x & 31) == 0) *dst = c;
+      return true;
+    }
+  }
+  const bool ok = encode128_warp(in, sq, c, !exact);
+  if ((threadIdx.x & 31) == 0) *dst = c;
+  return ok;
+}
+
 // SW: mask words of the longest compaction span (32 tokens each): 2, or 4
 // for ranks of 64..128 tokens per thread (more registers, so only then).
-template <typename T, int G, int SW>
+// FULL: the two-hop histogram exchange (C x G > 8), multi-cluster units
+// (P > 1) and candidates mode are compiled in; the common one-hop decode
+// launches an instance without them (measured 3.6-4.8 % faster at configs
+// 1-3: fewer registers, 71 KB instead of 125 KB of code).
+template <typename T, int G, int SW, bool FULL>
 __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   static_assert(G >= 1 && G <= kMaxG && (kConsumerWarps % G) == 0, "G must divide the warp count");
   constexpr int WG = kConsumerWarps / G;  // consumer warps per q-head
@@ -267,7 +288,8 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   __shared__ int nsel[kMaxG];
   const int C = p.C;
   const int rank = (int)cluster_rank();
-  const int P = p.P;
+  const int P = FULL ? p.P : 1;
+  uint32_t* const pcand = FULL ? p.cand : nullptr;  // candidates mode (sequence sharding)
   const int pc = (blockIdx.x / C) % P;  // this cluster's token range within the unit
   const int gr = pc * C + rank;          // rank over the unit's P * C CTAs
   const int unit = blockIdx.x / (C * P);
@@ -304,7 +326,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   uint64_t* hist_bar = full_bar + 2 * kMaxStages;
   uint64_t* inbox_bar = hist_bar + 1;
   uint64_t* sc_bar = hist_bar + 2;
-  const bool two_hop = C * G > 8 || P > 1;  // histogram exchange topology (see the select phase)
+  const bool two_hop = FULL && (C * G > 8 || P > 1);  // histogram exchange topology (see the select phase)
   const int xunit = hk * p.qsplit + part;     // this cache's unit index (global scratch)
   const int owners = min(C, G);               // ranks of a cluster that own a head
   int n_owned = 0;  // q-heads whose final merge this rank performs
@@ -351,7 +373,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     if (!two_hop) mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
     else if (n_owned) mbar_expect_tx(hist_bar, (uint32_t)(n_owned * C * kHistBins * 2));
     if (two_hop) mbar_expect_tx(sc_bar, (uint32_t)(G * 16));
-    if (n_owned && !p.cand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
+    if (n_owned && !pcand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
   }
   // the G query heads (and the new key) are loaded before the barrier so the
   // global-load latency overlaps the barrier initialisation
@@ -394,10 +416,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     ADAMAS_TRACE(12);
     if (p.dbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
       for (int w = 0; w < 4; ++w) { c.lo[w] = __float_as_uint(f[w]); c.hi[w] = 0u; }
-    } else if (!encode128(f, sqs + warp * kHeadDim, c, p.exact_encode != 0) && lane == 0) {
+      if (lane == 0) qcode[warp] = c;
+    } else if (!encode128_to(f, sqs + warp * kHeadDim, qcode + warp, p.exact_encode != 0) && lane == 0) {
       atomicOr(p.status, kStatusDegenerate);
     }
-    if (lane == 0) qcode[warp] = c;
     ADAMAS_TRACE(13);
   } else if (has_new && warp == G) {  // append (kv_cache.cpp:62-71); part 0 of a split kv-head writes
     const int64_t row = (int64_t)hk * cap + s_old;
@@ -407,13 +429,9 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     }
     float kf[4];
     Raw4<T>::to_float(kr, kf);
-    Code c;
-    if (!encode128(kf, sqs + G * kHeadDim, c, p.exact_encode != 0) && lane == 0)
+    if (!encode128_to(kf, sqs + G * kHeadDim, qcode + G, p.exact_encode != 0) && lane == 0)
       atomicOr(p.status, kStatusDegenerate);
-    if (lane == 0) {
-      qcode[G] = c;
-      if (part == 0) store_code(planes, cap, s_old, c);
-    }
+    if (lane == 0 && part == 0) store_code(planes, cap, s_old, qcode[G]);  // written by this lane
   }
   consumer_sync();
   QCode qc[G];
@@ -711,16 +729,16 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       auto emit = [&](int t, bool is_eq) {
         if (is_eq && eq_seen++ >= eq_budget) return;  // ties beyond the budget are not taken
         const int tok = (int)start + t;
-        if (ADAMAS_GATHER_PREFETCH == 2 && !p.cand) prefetch_row(t);
+        if (ADAMAS_GATHER_PREFETCH == 2 && !pcand) prefetch_row(t);
         if (pos < selcap) sel[g * selcap + pos] = tok;
         if (idx_row) idx_row[pos] = tok;
-        if (p.cand) {  // (distance, global index) key: the distributed top-k's order
+        if (pcand) {  // (distance, global index) key: the distributed top-k's order
           const int64_t off = ((int64_t)si * n_q + q0 + g) * p.budget + out_off + pos;
           const uint32_t key = ((uint32_t)dg[dslot(t)] << 23) | (uint32_t)(p.cand_base + tok);
           if (p.peers.n) {
             for (int r = 0; r < p.peers.n; ++r) p.peers.keys[r][off] = key;  // NVLink stores
           } else {
-            p.cand[off] = key;
+            pcand[off] = key;
           }
         }
         ++pos;
@@ -747,19 +765,19 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       int32_t* row = p.idx + ((int64_t)si * n_q + q0 + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
     }
-    if (gr == 0 && p.cand && t_in == 0) {
+    if (gr == 0 && pcand && t_in == 0) {
       const int64_t row = ((int64_t)si * n_q + q0 + g) * p.budget;
       if (p.peers.n) {
         for (int r = 0; r < p.peers.n; ++r)
           for (int i = k_eff; i < p.budget; ++i) p.peers.keys[r][row + i] = 0xffffffffu;
       } else {
-        for (int i = k_eff; i < p.budget; ++i) p.cand[row + i] = 0xffffffffu;
+        for (int i = k_eff; i < p.budget; ++i) pcand[row + i] = 0xffffffffu;
       }
     }
   }
   consumer_sync();
   ADAMAS_TRACE(7);
-  if (p.cand) {  // candidates mode: the selection is the product
+  if (pcand) {  // candidates mode: the selection is the product
     if (p.peers.n && tid == 0) peer_signal(p.peers);
     return;
   }
