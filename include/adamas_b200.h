@@ -308,7 +308,9 @@ int adamas_attention_f64(const double* queries, const double* keys, const double
 
 /* ---------------------------------------------------------------- diagnostics
  * Subsequent fused decode launches write up to 16 %globaltimer stamps per CTA
- * (phase boundaries) into device_buffer[blockIdx * 16 + i]; NULL disables. */
+ * (phase boundaries) into device_buffer[blockIdx * 16 + i]; NULL disables.
+ * Effective only in a diagnostics build of the library (ADAMAS_DIAG=1,
+ * `python paper_2510_18413_b200/build.py --diag`); a no-op otherwise. */
 void adamas_debug_trace(unsigned long long* device_buffer);
 
 /* ---------------------------------------------------------------- host converters */

@@ -37,6 +37,9 @@ namespace adamas_dev {
 #ifndef ADAMAS_SPAN_MASKS
 #define ADAMAS_SPAN_MASKS 1  // compaction: register span masks over a swizzled layout (1) or 32-token groups (0)
 #endif
+#ifndef ADAMAS_DIAG
+#define ADAMAS_DIAG 0  // 1: phase stamps and timing-only switches (ADAMAS_DBG) compiled in (build.py --diag)
+#endif
 #ifndef ADAMAS_GATHER_PREFETCH
 #define ADAMAS_GATHER_PREFETCH 2  // L2-prefetch the gather rows: 1 all rows <= T in the count pass, 2 survivors in the emit, 0 none
 #endif
@@ -114,10 +117,10 @@ __device__ __forceinline__ unsigned long long trace_clock(int dbg) {
 // shared load forces the wait.
 #define ADAMAS_TRACE(i)                                                                 \
   do {                                                                                  \
-    if (p.trace != nullptr && threadIdx.x == kTraceTid && ((p.dbg >> 8) & 31) == (i) + 1) { \
+    if (ptrace != nullptr && threadIdx.x == kTraceTid && ((pdbg >> 8) & 31) == (i) + 1) {   \
       __shared__ volatile int trace_sink;                                               \
       const int sink = trace_sink;                                                      \
-      p.trace[blockIdx.x * 16 + (i)] = trace_clock(p.dbg) + (unsigned long long)(sink & 0); \
+      ptrace[blockIdx.x * 16 + (i)] = trace_clock(pdbg) + (unsigned long long)(sink & 0);   \
     }                                                                                   \
   } while (0)
 
@@ -289,6 +292,9 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   const int C = p.C;
   const int rank = (int)cluster_rank();
   const int P = FULL ? p.P : 1;
+  // diagnostics (phase stamps, timing-only switches) exist only in ADAMAS_DIAG builds
+  const int pdbg = ADAMAS_DIAG ? p.dbg : 0;
+  unsigned long long* const ptrace = ADAMAS_DIAG ? p.trace : nullptr;
   uint32_t* const pcand = FULL ? p.cand : nullptr;  // candidates mode (sequence sharding)
   const int pc = (blockIdx.x / C) % P;  // this cluster's token range within the unit
   const int gr = pc * C + rank;          // rank over the unit's P * C CTAs
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   // ---------------------------------------------------------------- prologue
   ADAMAS_TRACE(0);
   // (taken by the producer lane: a globaltimer read stalls the reading warp's fp64 work)
-  if (p.trace != nullptr && tid == kConsumers && !(p.dbg & 32)) p.trace[blockIdx.x * 16 + 14] = trace_clock(p.dbg);
+  if (ptrace != nullptr && tid == kConsumers && !(pdbg & 32)) ptrace[blockIdx.x * 16 + 14] = trace_clock(pdbg);
   // Tokens >= clean_local may still be in flight from the preceding kernel
   // (its append): stages reaching them are issued after the PDL wait.
   const int clean_local = (int)max((int64_t)0, min((int64_t)mem_len, p.seq[si].clean - start));
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 
   if (warp == kProducerWarp) {  // keep the ring full: refill a slot once all consumer warps released it
     if (lane == 0) {
-      if (p.dbg & 4) __nanosleep(8000);  // diagnostics: keep the producer off the SMSP during the prologue
+      if (pdbg & 4) __nanosleep(8000);  // diagnostics: keep the producer off the SMSP during the prologue
       for (int st = ring; st < n_stages; ++st) {
         const int slot = st % ring;
         mbar_wait_backoff(&empty_bar[slot], (uint32_t)((st / ring) - 1) & 1u);
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     *reinterpret_cast<float4*>(qfs + warp * kHeadDim + lane * 4) = make_float4(f[0], f[1], f[2], f[3]);
     Code c;
     ADAMAS_TRACE(12);
-    if (p.dbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
+    if (pdbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
       for (int w = 0; w < 4; ++w) { c.lo[w] = __float_as_uint(f[w]); c.hi[w] = 0u; }
       if (lane == 0) qcode[warp] = c;
     } else if (!encode128_to(f, sqs + warp * kHeadDim, qcode + warp, p.exact_encode != 0) && lane == 0) {
@@ -719,7 +725,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     if (t_in == 0) nsel[g] = min(lt_tot + min(eq_tot, eq_budget), selcap);
     ADAMAS_TRACE(6);
     if (my_lt > 0 || (my_eq > 0 && eq_before < eq_budget)) {
-      int32_t* idx_row = (p.idx && !(p.dbg & 2))
+      int32_t* idx_row = (p.idx && !(pdbg & 2))
                              ? p.idx + ((int64_t)si * n_q + q0 + g) * p.budget + out_off
                              : nullptr;
       int pos = lt_before + min(eq_before, eq_budget);
@@ -940,7 +946,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     }
   }
   ADAMAS_TRACE(11);
-  if (p.trace != nullptr && tid == kTraceTid && !(p.dbg & 32)) p.trace[blockIdx.x * 16 + 15] = trace_clock(p.dbg);
+  if (ptrace != nullptr && tid == kTraceTid && !(pdbg & 32)) ptrace[blockIdx.x * 16 + 15] = trace_clock(pdbg);
 }
 
 }  // namespace adamas_dev

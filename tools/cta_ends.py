@@ -6,6 +6,13 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["ADAMAS_DBG"] = "64"
+# phase stamps exist only in the diagnostics build (build.py --diag)
+_diag = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_18413_b200",
+                     "libadamas_b200_diag.so")
+if "ADAMAS_LIB" not in os.environ:
+    if not os.path.exists(_diag):
+        sys.exit("needs the diagnostics build: python paper_2510_18413_b200/build.py --diag")
+    os.environ["ADAMAS_LIB"] = _diag
 import torch  # noqa: E402
 
 import paper_2510_18413_b200 as ad  # noqa: E402

@@ -1,5 +1,7 @@
 import os, sys, ctypes as C
 sys.path.insert(0, os.getcwd())
+# phase stamps exist only in the diagnostics build (build.py --diag)
+os.environ.setdefault("ADAMAS_LIB", os.path.join(os.getcwd(), "paper_2510_18413_b200", "libadamas_b200_diag.so"))
 import torch
 import paper_2510_18413_b200 as ad
 from paper_2510_18413_b200._lib import load

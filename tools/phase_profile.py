@@ -15,6 +15,13 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# phase stamps exist only in the diagnostics build (build.py --diag)
+_diag = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_18413_b200",
+                     "libadamas_b200_diag.so")
+if "ADAMAS_LIB" not in os.environ:
+    if not os.path.exists(_diag):
+        sys.exit("needs the diagnostics build: python paper_2510_18413_b200/build.py --diag")
+    os.environ["ADAMAS_LIB"] = _diag
 import torch  # noqa: E402
 
 ap = argparse.ArgumentParser()
