@@ -211,27 +211,28 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
   return ADAMAS_OK;
 }
 
+// Instance choice: FULL only where the launch needs the two-hop exchange,
+// multi-cluster units or candidates mode; the compaction form SW from the
+// rank length (spans cover it with 2 or 4 mask words, else 32-token groups).
+template <typename T, int G>
+int launch_fused_g(const FusedParams& prm, int C, size_t smem, cudaStream_t s, bool full, int sw) {
+  if (full) return sw == 2 ? launch_fused_t<T, G, 2, true>(prm, C, smem, s) : launch_fused_t<T, G, 0, true>(prm, C, smem, s);
+  if (sw == 2) return launch_fused_t<T, G, 2, false>(prm, C, smem, s);
+  if (sw == 4) return launch_fused_t<T, G, 4, false>(prm, C, smem, s);
+  return launch_fused_t<T, G, 0, false>(prm, C, smem, s);
+}
+
 template <typename T>
 int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaStream_t s) {
-  // 4-word compaction spans only where a rank needs 64..128 tokens per thread
-  const int nt = kConsumers / G;
-  const bool wide = (int64_t)prm.chunk > (int64_t)nt * 64 && (int64_t)prm.chunk <= (int64_t)nt * 128;
-  // the full instance (two-hop exchange, multi-cluster units, candidates)
-  // only where the launch needs it
+  const int64_t nt = kConsumers / G;
+  const int sw = prm.chunk <= nt * 64 ? 2 : prm.chunk <= nt * 128 ? 4 : 0;
   const bool full = prm.P > 1 || prm.cand != nullptr || C * G > 8;
   switch (G) {
-    case 1:
-      return full ? launch_fused_t<T, 1, 2, true>(prm, C, smem, s)
-                  : wide ? launch_fused_t<T, 1, 4, false>(prm, C, smem, s) : launch_fused_t<T, 1, 2, false>(prm, C, smem, s);
-    case 2:
-      return full ? launch_fused_t<T, 2, 2, true>(prm, C, smem, s)
-                  : wide ? launch_fused_t<T, 2, 4, false>(prm, C, smem, s) : launch_fused_t<T, 2, 2, false>(prm, C, smem, s);
-    case 4:
-      return full ? launch_fused_t<T, 4, 2, true>(prm, C, smem, s)
-                  : wide ? launch_fused_t<T, 4, 4, false>(prm, C, smem, s) : launch_fused_t<T, 4, 2, false>(prm, C, smem, s);
-    case 8:
-      return full ? launch_fused_t<T, 8, 2, true>(prm, C, smem, s)
-                  : wide ? launch_fused_t<T, 8, 4, false>(prm, C, smem, s) : launch_fused_t<T, 8, 2, false>(prm, C, smem, s);
+    case 1: return launch_fused_g<T, 1>(prm, C, smem, s, full, sw);
+    case 2: return launch_fused_g<T, 2>(prm, C, smem, s, full, sw);
+    case 4: return launch_fused_g<T, 4>(prm, C, smem, s, full, sw);
+    case 8:  // test shapes only: one instance per mode, 32-token groups
+      return full ? launch_fused_t<T, 8, 0, true>(prm, C, smem, s) : launch_fused_t<T, 8, 0, false>(prm, C, smem, s);
   }
   return kFusedUnsupported;
 }

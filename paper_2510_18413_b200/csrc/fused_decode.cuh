@@ -34,9 +34,6 @@
 
 namespace adamas_dev {
 
-#ifndef ADAMAS_SPAN_MASKS
-#define ADAMAS_SPAN_MASKS 1  // compaction: register span masks over a swizzled layout (1) or 32-token groups (0)
-#endif
 #ifndef ADAMAS_DIAG
 #define ADAMAS_DIAG 0  // 1: phase stamps and timing-only switches (ADAMAS_DBG) compiled in (build.py --diag)
 #endif
@@ -271,8 +268,11 @@ __device__ __forceinline__ bool encode128_to(const float in[4], double* sq, Code
   return ok;
 }
 
-// SW: mask words of the longest compaction span (32 tokens each): 2, or 4
-// for ranks of 64..128 tokens per thread (more registers, so only then).
+// SW: compaction form, fixed per launch from the rank length: 2 or 4 = spans
+// of up to 64 or 128 tokens per thread with that many mask words (4 costs
+// registers, so only where needed), 0 = 32-token groups per thread for ranks
+// longer than that. Each instance carries one form only (measured: 1.6 %
+// faster than choosing at run time).
 // FULL: the two-hop histogram exchange (C x G > 8), multi-cluster units
 // (P > 1) and candidates mode are compiled in; the common one-hop decode
 // launches an instance without them (measured 3.6-4.8 % faster at configs
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   const int span_groups = (len + 31) >> 5;
   int sh = 0;
   while ((2 << sh) < 4 * SW && (NT << (4 + sh)) < span_groups * 32) ++sh;
-  const bool span = ADAMAS_SPAN_MASKS && (NT << (4 + sh)) >= span_groups * 32;  // CTA-uniform
+  constexpr bool span = SW > 0;  // the launcher picks SW so that spans cover the rank
   const int nch = 2 << sh;  // 16-B chunks (8 tokens) per span
   auto swz = [&](int sp) { return nch >= 8 ? (sp & 7) : ((sp * nch) >> 3) & (nch - 1); };
   // shared-memory slot of local token x in a head's distance row; for
@@ -663,9 +663,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     const T* Kg = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
     const T* Vg = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
     const int tok0 = t_in << (4 + sh);
-    uint32_t sl[SW], se[SW];  // span masks: bit i of word w = token tok0 + 32 w + i
+    constexpr int NW = SW > 0 ? SW : 1;
+    uint32_t sl[NW], se[NW];  // span masks: bit i of word w = token tok0 + 32 w + i
 #pragma unroll
-    for (int w = 0; w < SW; ++w) sl[w] = se[w] = 0u;
+    for (int w = 0; w < NW; ++w) sl[w] = se[w] = 0u;
     // warm L2 for the gather, one prefetch per 128-B line: each survivor as
     // the emit places it (default), or every row at distance <= T in the
     // count pass (ADAMAS_GATHER_PREFETCH = 1)

@@ -185,10 +185,10 @@ def test_fused_decode_exchange_topologies(gpu, oracle, monkeypatch, cluster, G):
 
 
 @pytest.mark.parametrize("S,G", [(8000, 1), (16000, 1), (32000, 1), (40000, 1),
-                                 (2000, 4), (4000, 4), (8000, 4), (9000, 4)])
+                                 (70000, 1), (2000, 4), (4000, 4), (8000, 4), (9000, 4), (20000, 4)])
 def test_fused_compaction_span_sizes(gpu, oracle, monkeypatch, S, G):
-    """one CTA per unit, so the rank length picks the compaction form: register
-    masks over 16 / 32 / 64-token spans per thread, or 32-token groups beyond"""
+    """one CTA per unit, so the rank length picks the compaction instance:
+    16..64-token spans (SW 2), 128-token spans (SW 4), or 32-token groups (SW 0)"""
     monkeypatch.setenv("ADAMAS_CLUSTER", "1")
     run_decode(gpu, oracle, S, 1, G, 128, True, seed=S + 13 * G, steps=2)
 
