@@ -279,6 +279,39 @@ def test_fast_encode_near_ties_and_scales(gpu, oracle):
         cache.truncate(S - 1)
 
 
+@pytest.mark.parametrize("cluster", ["1", "4"])
+def test_uncertified_appended_key(gpu, oracle, monkeypatch, cluster):
+    """Appended keys built to sit on the +/- kQ28 sigma thresholds (the fp32
+    certificate fails): the fused step takes the exact code (at G = 1 from the
+    helper warp, after the scan), stores it in the cache and selects with it."""
+    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    rng = np.random.default_rng(9)
+    S, budget = 3000, 64
+    K, V, q = make_inputs(S, 1, 1, False, 43)
+    H = np.array([[1.0]])
+    for _ in range(7):
+        H = np.block([[H, H], [H, -H]])
+    H /= np.sqrt(128.0)
+    cache = fill_cache(gpu, K[:-1], V[:-1], False, capacity=S + 64)
+    for trial in range(12):
+        y = rng.standard_normal(128)
+        sigma = np.sqrt(np.mean(y * y))
+        y[(5 * trial) % 128] = 0.6744897501960817 * sigma * (1 if trial % 2 else -1)
+        k = (H @ y).astype(np.float32).reshape(1, 1, 128)
+        # the query close to the key, so the appended token competes for the selection
+        qq = (k[0] + 0.05 * rng.standard_normal((1, 128))).astype(np.float32)
+        out, idx = cache.decode_step(to_dev(qq, False), to_dev(k[0], False), to_dev(V[-1], False), budget)
+        Kt = np.concatenate([K[:-1], k])
+        Vt = np.concatenate([V[:-1], V[-1:]])
+        _, _, eidx, eout = oracle_decode(oracle, Kt, Vt, qq, budget)
+        assert np.array_equal(idx.cpu().numpy(), eidx), trial
+        assert rel_err(out.cpu().numpy(), eout).max() <= TOL[False], trial
+        words = cache.code_words().cpu().numpy().view(np.uint16)
+        assert np.array_equal(words[0][S - 1], oracle.encode_pack_rows(k[:, 0].astype(np.float64))[0]), trial
+        assert cache.status() == 0
+        cache.truncate(S - 1)
+
+
 @pytest.mark.parametrize("metric,bits,ref_metric", [("euclidean_sq", 2, 1), ("hamming_1bit", 1, 0)])
 def test_ablation_metrics_match_reference(gpu, reference, metric, bits, ref_metric):
     """SURVEY 8f row f4: Metric::euclidean_sq over 2-bit codes and the 1-bit
