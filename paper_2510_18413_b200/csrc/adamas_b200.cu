@@ -160,9 +160,9 @@ int ensure_unit_scratch(adamas_cache* c, size_t slots) {
 }
 
 // ----------------------------------------------------------------- fused launcher
-template <typename T, int G, int SW, bool FULL>
+template <typename T, int G, int SW, bool FULL, int CT = 0>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
-  auto kern = fused_decode_kernel<T, G, SW, FULL>;
+  auto kern = fused_decode_kernel<T, G, SW, FULL, CT>;
   static bool configured = false;
   static size_t configured_smem = 0;
   if (!configured || configured_smem < smem) {
@@ -217,7 +217,7 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
 template <typename T, int G>
 int launch_fused_g(const FusedParams& prm, int C, size_t smem, cudaStream_t s, bool full, int sw) {
   if (full) return sw == 2 ? launch_fused_t<T, G, 2, true>(prm, C, smem, s) : launch_fused_t<T, G, 0, true>(prm, C, smem, s);
-  if (sw == 2) return launch_fused_t<T, G, 2, false>(prm, C, smem, s);
+  if (sw == 2) return C == 4 ? launch_fused_t<T, G, 2, false, 4>(prm, C, smem, s) : launch_fused_t<T, G, 2, false>(prm, C, smem, s);
   if (sw == 4) return launch_fused_t<T, G, 4, false>(prm, C, smem, s);
   return launch_fused_t<T, G, 0, false>(prm, C, smem, s);
 }

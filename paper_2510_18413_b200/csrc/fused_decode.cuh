@@ -277,7 +277,9 @@ __device__ __forceinline__ bool encode128_to(const float in[4], double* sq, Code
 // (P > 1) and candidates mode are compiled in; the common one-hop decode
 // launches an instance without them (measured 3.6-4.8 % faster at configs
 // 1-3: fewer registers, 71 KB instead of 125 KB of code).
-template <typename T, int G, int SW, bool FULL>
+// CT: the cluster size when fixed at compile time (the common C = 4 decode
+// launch; measured 3 % faster), 0 = from the launch parameters.
+template <typename T, int G, int SW, bool FULL, int CT>
 __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   static_assert(G >= 1 && G <= kMaxG && (kConsumerWarps % G) == 0, "G must divide the warp count");
   constexpr int WG = kConsumerWarps / G;  // consumer warps per q-head
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   __shared__ int rank_cnt[16][2];              // two-hop exchange, owner side: per rank (< T, == T)
   __shared__ int cl_cnt[2];                    // multi-cluster unit: earlier clusters' (< T, == T)
   __shared__ int nsel[kMaxG];
-  const int C = p.C;
+  const int C = CT > 0 ? CT : p.C;
   const int rank = (int)cluster_rank();
   const int P = FULL ? p.P : 1;
   // diagnostics (phase stamps, timing-only switches) exist only in ADAMAS_DIAG builds
