@@ -218,7 +218,7 @@ template <typename T, int G>
 int launch_fused_g(const FusedParams& prm, int C, size_t smem, cudaStream_t s, bool full, int sw) {
   if (full) return sw == 2 ? launch_fused_t<T, G, 2, true>(prm, C, smem, s) : launch_fused_t<T, G, 0, true>(prm, C, smem, s);
   if (sw == 2) return C == 4 ? launch_fused_t<T, G, 2, false, 4>(prm, C, smem, s) : launch_fused_t<T, G, 2, false>(prm, C, smem, s);
-  if (sw == 4) return launch_fused_t<T, G, 4, false>(prm, C, smem, s);
+  if (sw == 4) return C == 1 ? launch_fused_t<T, G, 4, false, 1>(prm, C, smem, s) : launch_fused_t<T, G, 4, false>(prm, C, smem, s);
   return launch_fused_t<T, G, 0, false>(prm, C, smem, s);
 }
 
