@@ -467,9 +467,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 
   // ---------------------------------------------------------------- scan
   ADAMAS_TRACE(2);
+  int slot = 0;
+  uint32_t phase = 0u;  // slot = st % ring, phase = (st / ring) & 1, kept incrementally
   for (int st = 0; st < n_stages; ++st) {
-    const int slot = st % ring;
-    mbar_wait(&full_bar[slot], (uint32_t)(st / ring) & 1u);
+    mbar_wait(&full_bar[slot], phase);
     const uint4* slo = stage + (size_t)slot * (kStageBytes / 16);
     const uint4* sx = slo + kStageTok;
     const int base = st * kStageTok;
@@ -499,6 +500,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
           atomicAdd(&hist[g * kHistBins + d[u][g]], 1);
         }
       }
+    }
+    if (++slot == ring) {
+      slot = 0;
+      phase ^= 1u;
     }
   }
   if (has_new && tid < G) {  // the appended token is a candidate
