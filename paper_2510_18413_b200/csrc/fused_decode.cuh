@@ -353,8 +353,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   // (its append): stages reaching them are issued after the PDL wait.
   const int clean_local = (int)max((int64_t)0, min((int64_t)mem_len, p.seq[si].clean - start));
   bool waited = !p.pdl;
-  auto issue = [&](int st) {
-    const int slot = st % ring;
+  auto issue = [&](int st, int slot) {  // slot = st % ring
     const int ntok = min(kStageTok, mem_len - st * kStageTok);
     if (!waited && st * kStageTok + ntok > clean_local) {
       grid_dependency_wait();
@@ -375,7 +374,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     mbar_init(inbox_bar, 1);
     mbar_init(sc_bar, 1);
     mbar_fence_init();
-    for (int st = 0; st < min(ring, n_stages); ++st) issue(st);
+    for (int st = 0; st < min(ring, n_stages); ++st) issue(st, st);
     // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
     // C partials per q-head it merges
     if (!two_hop) mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
@@ -409,10 +408,15 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   if (warp == kProducerWarp) {  // keep the ring full: refill a slot once all consumer warps released it
     if (lane == 0) {
       if (pdbg & 4) __nanosleep(8000);  // diagnostics: keep the producer off the SMSP during the prologue
+      int slot = 0;
+      uint32_t phase = 0u;  // of the slot's previous use: ((st / ring) - 1) & 1
       for (int st = ring; st < n_stages; ++st) {
-        const int slot = st % ring;
-        mbar_wait_backoff(&empty_bar[slot], (uint32_t)((st / ring) - 1) & 1u);
-        issue(st);
+        mbar_wait_backoff(&empty_bar[slot], phase);
+        issue(st, slot);
+        if (++slot == ring) {
+          slot = 0;
+          phase ^= 1u;
+        }
       }
     }
     return;
