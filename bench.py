@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=11)
+    ap.add_argument("--no-check", action="store_true",
+                    help="skip the oracle check of the last timed step (default: checked, outside the timed region)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="seqshard1m at N > 1: peer-memory mailboxes (default) or NCCL all-gathers")
     a = ap.parse_args()
@@ -227,6 +229,38 @@ def _prefill(ad, torch, n_kv, S, dtype, gen, cap_extra=1):
     return c
 
 
+def parity_check(torch, caches, qs, out, idx, s_last, S, B, layers):
+    """Checker, outside every timed region (the oracle is test infrastructure
+    and is never measured): the LAST TIMED step's selection and output of the
+    given layers (request 0), as the timed graph left them, against the CPU
+    oracle over the cache contents that step saw (S tokens, the appended one
+    included). Indices bit-exact, output within the north-star tolerance."""
+    import numpy as np
+
+    from oracle.bindings import Oracle  # checker only
+    from tests.gpu_helpers import oracle_decode, rel_err
+
+    oracle = Oracle()
+    worst = 0.0
+    for l in layers:
+        c = caches[l][0]
+        K = c.keys()[:, :S].float().permute(1, 0, 2).contiguous().cpu().numpy()
+        V = c.values()[:, :S].float().permute(1, 0, 2).contiguous().cpu().numpy()
+        q = qs[s_last, l, 0].float().cpu().numpy()
+        _, _, eidx, eout = oracle_decode(oracle, K, V, q, B)
+        got_idx = idx[l, 0].cpu().numpy()
+        keep = min(B, S)
+        if not np.array_equal(got_idx[:, :keep], eidx):
+            bad = int((got_idx[:, :keep] != eidx).any(axis=1).sum())
+            return {"status": "MISMATCH", "detail": f"layer {l}: indices differ in {bad} of {q.shape[0]} heads"}
+        err = float(rel_err(out[l, 0].cpu().numpy(), eout).max())
+        worst = max(worst, err)
+        if err > (1e-2 if c.dtype == torch.bfloat16 else 1e-3):
+            return {"status": "MISMATCH", "detail": f"layer {l}: output rel err {err:.2e}"}
+    return {"status": "ok", "checked": f"last timed step, layers {list(layers)}, request 0, every q-head: indices "
+                                       f"bit-exact vs the oracle, max output rel err {worst:.2e}"}
+
+
 def _timed_graph(torch, dist, ws, body, steps, local, sample_clocks=False):
     """Capture `steps` calls of body(s, stream) in one CUDA graph, warm replay,
     then time one replay with CUDA events on the capture stream (max over
@@ -377,6 +411,17 @@ def run_ours(args):
     # device timeline); kernel time per launch is bounded by elapsed / launches.
     elapsed_ms, clocks = _timed_graph(torch, dist, ws, lambda s, st: step(args.warmup + s, st), args.steps, local,
                                       sample_clocks=True)
+    parity = None
+    if not args.no_check and not seqshard:  # every rank checks its own heads
+        parity = parity_check(torch, caches, qs, out, idx, args.warmup + args.steps - 1, S, B,
+                              sorted({0, L // 2, L - 1}))
+        if ws > 1:
+            bad = torch.tensor([0 if parity["status"] == "ok" else 1 + rank], device="cuda")
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            if int(bad[0]) and parity["status"] == "ok":
+                parity = {"status": "MISMATCH", "detail": f"on rank {int(bad[0]) - 1}"}
+            elif parity["status"] == "ok":
+                parity["checked"] += f"; every one of the {ws} ranks checked its own heads"
     launches_per_step = L * (3 if seqshard else 1)
     ms_per_step = elapsed_ms / args.steps
     tokens_per_layer = NS  # one decoded token per sequence per layer
@@ -498,8 +543,11 @@ def run_ours(args):
             "gpu_launches": args.steps * launches_per_step,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line))
+        if parity and parity["status"] != "ok":
+            raise SystemExit(f"parity check failed: {parity['detail']}")
     if ws > 1:
         dist.destroy_process_group()
 

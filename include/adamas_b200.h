@@ -47,7 +47,11 @@ extern "C" {
 #define ADAMAS_BF16 1
 
 /* Sticky device status bits. */
-#define ADAMAS_STATUS_DEGENERATE 1 /* a zero / non-finite vector was encoded */
+#define ADAMAS_STATUS_DEGENERATE 1     /* a zero / non-finite vector was encoded (quantizer.cpp:46-47) */
+#define ADAMAS_STATUS_SYNC_TIMEOUT 4   /* a multi-cluster unit barrier gave up: results invalid */
+#define ADAMAS_STATUS_PEER_TIMEOUT 8   /* a peer-memory exchange wait gave up: results invalid */
+#define ADAMAS_STATUS_BAD_SELECTION 16 /* sparse_attention: a row is empty, unsorted or out of range
+                                          (kv_cache.cpp:90-91, attention.cpp:42); nothing was read */
 
 typedef struct adamas_cache adamas_cache;
 
@@ -135,13 +139,18 @@ int adamas_score_metric(const adamas_cache* cache, const uint16_t* q_ref, int n_
 
 /* top_k(scores, k) per row (estimator.cpp:75-90): the k smallest under the
  * order (score, index), ascending indices. scores device int32 [n_rows][n]
- * (values must lie in [0, 65535]); idx device int32 [n_rows][k]; entries past
- * min(k, n) are set to -1. */
+ * (any int32 value, as the reference's DistanceScores); idx device int32
+ * [n_rows][k]; entries past min(k, n) are set to -1. */
 int adamas_topk(const int32_t* scores, int n_rows, int64_t n, int64_t k, int32_t* idx, void* stream);
 
 /* sparse_attention(q, cache, sel) per q-head (attention.cpp:40-45 = gather,
  * kv_cache.cpp:84-99, + full_attention, attention.cpp:8-38) in fp32:
- * idx device int32 [n_q_heads][k] strictly increasing (-1 entries end a row);
+ * idx device int32 [n_q_heads][k] strictly increasing (-1 entries end a row).
+ * The reference's gather preconditions (indices in range and strictly
+ * increasing, kv_cache.cpp:90-91) and its empty-selection check
+ * (attention.cpp:42) are validated on the device per row: a violating row is
+ * not read, its output is NaN and ADAMAS_STATUS_BAD_SELECTION is latched in
+ * the cache status (the facades raise ConfigError from it);
  * out device float32 [n_q_heads][128]; lse (optional, may be NULL) device
  * float32 [n_q_heads][2] = (row max logit, sum of exp) for log-sum-exp merges. */
 int adamas_sparse_attention(const adamas_cache* cache, const void* q, int n_q_heads,
@@ -312,6 +321,19 @@ int adamas_attention_f64(const double* queries, const double* keys, const double
  * Effective only in a diagnostics build of the library (ADAMAS_DIAG=1,
  * `python paper_2510_18413_b200/build.py --diag`); a no-op otherwise. */
 void adamas_debug_trace(unsigned long long* device_buffer);
+
+/* Launch-plan overrides for tests and tools (the automatic plan is the
+ * product default). values[i] for i < n, in order: qsplit (0 auto), cluster
+ * CTAs (0 auto), clusters per unit P (1), ring stages (0 auto), shared-memory
+ * cap in KB (0 auto), exact fp64 encode (0), diagnostics switches (0), no PDL
+ * (0), composed operators instead of the fused launch (0), require the fused
+ * launch (0). The initial values are read once from the ADAMAS_QSPLIT,
+ * ADAMAS_CLUSTER, ADAMAS_P, ADAMAS_STAGES, ADAMAS_SMEM_KB, ADAMAS_EXACT_ENCODE,
+ * ADAMAS_DBG, ADAMAS_NO_PDL, ADAMAS_NO_FUSED, ADAMAS_REQUIRE_FUSED environment
+ * variables at first use; nothing on the launch path reads the environment. */
+#define ADAMAS_TUNING_FIELDS 10
+int adamas_set_tuning(const int* values, int n);
+int adamas_get_tuning(int* values, int n);
 
 /* ---------------------------------------------------------------- host converters */
 

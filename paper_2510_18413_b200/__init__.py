@@ -8,6 +8,7 @@ from ._lib import ConfigError, AdamasRuntimeError, load  # noqa: F401
 
 load()
 
-from .adamas import KvCache, top_k, decode_step_batched, HEAD_DIM  # noqa: E402,F401
+from .adamas import KvCache, top_k, decode_step_batched, HEAD_DIM, tuning, set_tuning, get_tuning  # noqa: E402,F401
 
-__all__ = ["KvCache", "top_k", "decode_step_batched", "ConfigError", "AdamasRuntimeError", "HEAD_DIM"]
+__all__ = ["KvCache", "top_k", "decode_step_batched", "ConfigError", "AdamasRuntimeError", "HEAD_DIM", "tuning",
+           "set_tuning", "get_tuning"]

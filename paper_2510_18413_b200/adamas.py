@@ -19,11 +19,14 @@ of libadamas_b200.so.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import torch
 
-from ._lib import (ADAMAS_BF16, ADAMAS_F32, ADAMAS_STATUS_DEGENERATE, ConfigError, check, load)
+from ._lib import (ADAMAS_BF16, ADAMAS_F32, ADAMAS_STATUS_BAD_SELECTION, ADAMAS_STATUS_DEGENERATE,
+                   ADAMAS_STATUS_PEER_TIMEOUT, ADAMAS_STATUS_SYNC_TIMEOUT, TUNING_FIELDS, AdamasRuntimeError,
+                   ConfigError, check, load)
 
 HEAD_DIM = 128
 _DTYPES = {torch.float32: ADAMAS_F32, torch.bfloat16: ADAMAS_BF16}
@@ -117,10 +120,23 @@ class KvCache:
         check(self.L.adamas_cache_status(self.h, _stream(stream), C.byref(s)))
         return s.value
 
+    def raise_on_status(self, stream=None) -> None:
+        """Reads and clears the sticky status word; raises what the reference
+        would have thrown: ConfigError for a zero / non-finite vector
+        (quantizer.cpp:46-47) or a bad gather (kv_cache.cpp:90-91,
+        attention.cpp:42), a runtime error for a timed-out exchange."""
+        st = self.status(stream)
+        if st & ADAMAS_STATUS_BAD_SELECTION:
+            raise ConfigError("KvCache: gather indices must be strictly increasing and in range "
+                              "(or the selection is empty)")
+        if st & ADAMAS_STATUS_DEGENERATE:
+            raise ConfigError("degenerate scale: zero or non-finite vector encoded")
+        if st & (ADAMAS_STATUS_SYNC_TIMEOUT | ADAMAS_STATUS_PEER_TIMEOUT):
+            raise AdamasRuntimeError(f"device exchange timed out (status {st:#x}): results invalid")
+
     def raise_on_degenerate(self, stream=None) -> None:
         """quantizer.cpp:46-47: a zero / non-finite vector is a ConfigError."""
-        if self.status(stream) & ADAMAS_STATUS_DEGENERATE:
-            raise ConfigError("degenerate scale: zero or non-finite vector encoded")
+        self.raise_on_status(stream)
 
     # -- operators ----------------------------------------------------------------
     def update(self, keys: torch.Tensor, values: torch.Tensor, stream=None) -> int:
@@ -169,8 +185,13 @@ class KvCache:
                                          _stream(stream)))
         return out
 
-    def sparse_attention(self, q: torch.Tensor, idx: torch.Tensor, with_lse: bool = False, stream=None):
-        """fp32 [n_q][128]; idx int32 [n_q][k] ascending (-1 ends a row)."""
+    def sparse_attention(self, q: torch.Tensor, idx: torch.Tensor, with_lse: bool = False, validate: bool = True,
+                         stream=None):
+        """fp32 [n_q][128]; idx int32 [n_q][k] ascending (-1 ends a row).
+
+        Rows are validated on the device (strictly increasing, in range, not
+        empty); with validate=True (the reference's behaviour) a bad row raises
+        ConfigError here, which synchronizes the stream."""
         _need(q, self.dtype, (self.head_dim,), "sparse_attention q")
         n_q = q.numel() // self.head_dim
         idx = idx.to(torch.int32).contiguous()
@@ -178,6 +199,8 @@ class KvCache:
         lse = torch.empty((n_q, 2), dtype=torch.float32, device="cuda") if with_lse else None
         check(self.L.adamas_sparse_attention(self.h, _ptr(q), n_q, _ptr(idx), idx.shape[-1], _ptr(out),
                                              _ptr(lse), _stream(stream)))
+        if validate:
+            self.raise_on_status(stream)
         return (out, lse) if with_lse else out
 
     def decode_step(self, q, k_new, v_new, budget: int, want_idx: bool = True, out=None, idx=None,
@@ -205,6 +228,34 @@ def top_k(scores: torch.Tensor, k: int, stream=None) -> torch.Tensor:
     out = torch.empty((s.shape[0], k), dtype=torch.int32, device="cuda")
     check(L.adamas_topk(_ptr(s), s.shape[0], s.shape[1], k, _ptr(out), _stream(stream)))
     return out
+
+
+def get_tuning() -> dict:
+    vals = (C.c_int * len(TUNING_FIELDS))()
+    check(load().adamas_get_tuning(vals, len(TUNING_FIELDS)))
+    return dict(zip(TUNING_FIELDS, list(vals)))
+
+
+def set_tuning(**kw) -> None:
+    """Launch-plan overrides (include/adamas_b200.h adamas_set_tuning)."""
+    cur = get_tuning()
+    for k, v in kw.items():
+        if k not in cur:
+            raise ConfigError(f"unknown tuning field {k}")
+        cur[k] = int(v)
+    vals = (C.c_int * len(TUNING_FIELDS))(*[cur[f] for f in TUNING_FIELDS])
+    check(load().adamas_set_tuning(vals, len(TUNING_FIELDS)))
+
+
+@contextlib.contextmanager
+def tuning(**kw):
+    """Temporarily override launch-plan fields: `with tuning(cluster=4): ...`."""
+    saved = get_tuning()
+    set_tuning(**kw)
+    try:
+        yield
+    finally:
+        set_tuning(**saved)
 
 
 def decode_step_batched(caches, q, k_new, v_new, budget, out=None, idx=None, want_idx=True, stream=None):

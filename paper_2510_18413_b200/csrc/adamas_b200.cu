@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <fstream>
+#include <list>
 #include <mutex>
 #include <cstdlib>
 #include <cstring>
@@ -72,14 +73,18 @@ size_t elem_size(int dtype) { return dtype == ADAMAS_BF16 ? 2 : 4; }
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::mutex mu;
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
 }
 
 int check_cache(const adamas_cache* c) {
@@ -144,6 +149,58 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+// Launch-plan knobs. Read from the environment ONCE (first use); tests and
+// tools override them explicitly through adamas_set_tuning. Nothing on the
+// launch path reads the environment.
+struct Tuning {
+  int qsplit = 0, cluster = 0, P = 1, stages = 0, smem_kb = 0;
+  int exact_encode = 0, dbg = 0, no_pdl = 0, composed = 0, require_fused = 0;
+  unsigned generation = 0;  // bumped on every change: invalidates cached plans
+};
+std::mutex g_tuning_mu;
+Tuning& tuning_ref() {
+  static Tuning t = [] {
+    Tuning x;
+    x.qsplit = env_int("ADAMAS_QSPLIT", 0);
+    x.cluster = env_int("ADAMAS_CLUSTER", 0);
+    x.P = std::max(1, env_int("ADAMAS_P", 1));
+    x.stages = env_int("ADAMAS_STAGES", 0);
+    x.smem_kb = env_int("ADAMAS_SMEM_KB", 0);
+    x.exact_encode = env_int("ADAMAS_EXACT_ENCODE", 0);
+    x.dbg = env_int("ADAMAS_DBG", 0);
+    x.no_pdl = env_int("ADAMAS_NO_PDL", 0);
+    x.composed = env_int("ADAMAS_NO_FUSED", 0);
+    x.require_fused = env_int("ADAMAS_REQUIRE_FUSED", 0);
+    return x;
+  }();
+  return t;
+}
+Tuning tuning() {
+  std::lock_guard<std::mutex> lock(g_tuning_mu);
+  return tuning_ref();
+}
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// Per-device, per-kernel launch facts: the dynamic shared memory a kernel has
+// been configured for, and how many clusters of a (C, smem) shape co-reside.
+struct KernelFacts {
+  size_t smem_configured = 0;
+  std::vector<std::pair<std::pair<int, size_t>, int>> max_clusters;  // ((C, smem) -> clusters)
+};
+std::mutex g_facts_mu;
+KernelFacts& kernel_facts(const void* kern, int dev) {
+  static std::list<std::pair<std::pair<const void*, int>, KernelFacts>> facts;  // stable references
+  for (auto& f : facts)
+    if (f.first.first == kern && f.first.second == dev) return f.second;
+  facts.push_back({{kern, dev}, KernelFacts{}});
+  return facts.back().second;
+}
+
 // Global scratch of multi-cluster units (not during graph capture: the first
 // eager launch of a shape sizes it).
 int ensure_unit_scratch(adamas_cache* c, size_t slots) {
@@ -163,14 +220,7 @@ int ensure_unit_scratch(adamas_cache* c, size_t slots) {
 template <typename T, int G, int SW, bool FULL, int CT = 0>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
   auto kern = fused_decode_kernel<T, G, SW, FULL, CT>;
-  static bool configured = false;
-  static size_t configured_smem = 0;
-  if (!configured || configured_smem < smem) {
-    ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-    configured_smem = smem;
-  }
+  const int dev = current_device();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * prm.qsplit * prm.P * C));
   cfg.blockDim = dim3(kFusedThreads);
@@ -183,25 +233,31 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  int max_clusters = 0;  // clusters of this (C, smem) shape co-resident on this device
+  {
+    std::lock_guard<std::mutex> lock(g_facts_mu);
+    KernelFacts& kf = kernel_facts((const void*)kern, dev);
+    if (kf.smem_configured < smem) {
+      ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      kf.smem_configured = smem;
+    }
+    if (prm.pdl || prm.P > 1) {
+      for (auto& e : kf.max_clusters)
+        if (e.first.first == C && e.first.second == smem) max_clusters = e.second;
+      if (max_clusters == 0) {
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0)
+          max_clusters = -1;
+        kf.max_clusters.push_back({{C, smem}, max_clusters});
+      }
+    }
+  }
+  const int64_t clusters = (int64_t)prm.n_seqs * prm.n_kv * prm.qsplit * prm.P;
   // PDL only when every cluster is co-resident (one wave): dependents then
   // occupy only SMs this grid does not need.
-  static int max_clusters[17] = {0};
-  if (prm.pdl) {
-    if (max_clusters[C] == 0) {
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = -1;
-      max_clusters[C] = n;
-    }
-    if ((int64_t)prm.n_seqs * prm.n_kv * prm.qsplit * prm.P > max_clusters[C]) prm.pdl = 0;
-  }
-  if (prm.P > 1) {  // spin barriers between the clusters of a unit: every cluster must be resident at once
-    if (max_clusters[C] == 0) {
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = -1;
-      max_clusters[C] = n;
-    }
-    if ((int64_t)prm.n_seqs * prm.n_kv * prm.qsplit * prm.P > max_clusters[C]) return kFusedUnsupported;
-  }
+  if (prm.pdl && clusters > max_clusters) prm.pdl = 0;
+  // spin barriers between the clusters of a unit: every cluster must be resident at once
+  if (prm.P > 1 && clusters > max_clusters) return kFusedUnsupported;
   if (prm.pdl) {
     attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
@@ -237,130 +293,172 @@ int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaSt
   return kFusedUnsupported;
 }
 
+// A launch plan: how one decode step of a shape maps onto clusters.
+struct FusedPlan {
+  int ok = 0;  // 0: the shape does not fit the single-launch kernel
+  int qsplit = 1, G = 1, C = 1, P = 1, chunk = 0, stages = 0;
+  size_t smem = 0;
+};
 
-
-// Chooses the cluster size C (CTAs per (sequence, kv-head) unit) and the
-// per-rank chunk, then launches. Returns kFusedUnsupported when the shape does
-// not fit the single-launch kernel (the caller composes operators instead).
-int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n_q, int dtype, const void* q,
-                        const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
-                        cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0,
-                        int qsplit = 0, const PeerPush* peers = nullptr) {
-  if (qsplit == 0) {  // auto
-    // Clusters above 4 CTAs do not reach a full wave of co-resident CTAs on
-    // B200 (measured): take the smallest split of a kv-head's q-heads over
-    // clusters (each re-reads the codes) whose launch uses C <= 4.
-    qsplit = env_int("ADAMAS_QSPLIT", 0);
-    if (qsplit <= 0) {
-      const int G_all = n_q / n_kv;
-      int best = 1, best_c = 1 << 30;
-      for (int qs = 1; qs <= G_all; qs *= 2) {
-        if (G_all % qs) break;
-        const int c = fused_decode_launch(caches, n_seqs, n_kv, n_q, dtype, q, k_new, v_new, budget, out, idx, s,
-                                          append, cand, cand_base, -qs);  // probe: C with this split
-        if (c == kFusedUnsupported) continue;
-        if (c <= 4) { best = qs; best_c = c; break; }
-        if (c < best_c) { best = qs; best_c = c; }
-      }
-      // More than one wave of CTAs: splitting the q-heads beats splitting the
-      // tokens at the same CTA count (measured: 16 x 32K Llama batch, qsplit 1
-      // x C 2 101 us vs qsplit 2 x C 1 87 us per layer-step).
-      if (best_c > 1 && (int64_t)n_seqs * n_kv * best * best_c > sm_count() && G_all % (2 * best) == 0) {
-        const int c2 = fused_decode_launch(caches, n_seqs, n_kv, n_q, dtype, q, k_new, v_new, budget, out, idx, s,
-                                           append, cand, cand_base, -2 * best);
-        if (c2 != kFusedUnsupported && c2 < best_c) best *= 2;
-      }
-      qsplit = best;
-    }
-  }
-  const bool probe = qsplit < 0;
-  if (probe) qsplit = -qsplit;
+// C CTAs per (sequence, kv-head, q-split part) unit and the per-rank chunk
+// for a fixed q-split. P > 1 (opt-in) exchanges histograms and partials
+// through global memory with a self-resetting barrier; it is exact but
+// measured slower than splitting the q-heads (qsplit), so the automatic
+// choice grows C only.
+FusedPlan plan_for_split(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, const Tuning& tu) {
+  FusedPlan pl;
   const int G = n_q / (n_kv * qsplit);
-  if (G != 1 && G != 2 && G != 4 && G != 8) return kFusedUnsupported;
-  if (n_seqs > kMaxSeqs || budget > (1 << 20)) return kFusedUnsupported;
-  int64_t s_max = 0;
-  for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + append);
-  if (s_max < 1) s_max = 1;
+  if (n_q % (n_kv * qsplit) || (G != 1 && G != 2 && G != 4 && G != 8)) return pl;
+  if (n_seqs > kMaxSeqs || budget > (1 << 20)) return pl;
   const int units = n_seqs * n_kv * qsplit;
-  // C CTAs per cluster, P clusters per unit. P > 1 (opt-in, ADAMAS_P)
-  // exchanges histograms and partials through global memory with a
-  // self-resetting barrier; it is exact but measured slower than splitting
-  // the q-heads (qsplit), so the automatic choice grows C only.
-  int C = env_int("ADAMAS_CLUSTER", 0);
+  int C = tu.cluster;
   if (C <= 0) {
     C = 1;
     while (C < 16 && units * C * 2 <= sm_count()) C *= 2;
   }
-  int P = std::max(1, env_int("ADAMAS_P", 1));
-  auto grow = [&]() {  // more CTAs per unit; false when out of options
-    if (C < 16) { C *= 2; return true; }
-    return false;
-  };
+  const int P = std::max(1, tu.P);
   for (;;) {
     int64_t chunk = (s_max + (int64_t)C * P - 1) / ((int64_t)C * P);
     chunk = (chunk + 255) / 256 * 256;
     const int selcap = (int)std::min<int64_t>(budget, chunk);
     // one CTA per SM when the grid fits the machine, else two (always two
     // with the 8-warp build, so consecutive launches co-reside)
-    size_t smem_cap =
-        kCtasPerSm == 1 && (size_t)units * C * P <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
-    if (env_int("ADAMAS_SMEM_KB", 0) > 0) smem_cap = (size_t)env_int("ADAMAS_SMEM_KB", 0) * 1024;  // experiments
+    size_t smem_cap = kCtasPerSm == 1 && (size_t)units * C * P <= (size_t)sm_count() ? 220 * 1024 : 108 * 1024;
+    if (tu.smem_kb > 0) smem_cap = (size_t)tu.smem_kb * 1024;  // experiments
     const FusedSmem base(G, C, (int)chunk, selcap, 0, P);
     const int want = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (chunk + kStageTok - 1) / kStageTok));
-    int stages = env_int("ADAMAS_STAGES", 0);
+    int stages = tu.stages;
     if (stages <= 0) {
       stages = want;
       while (stages > 2 && base.total + (size_t)stages * kStageTok * 32 > smem_cap) --stages;
     }
     const FusedSmem L(G, C, (int)chunk, selcap, stages, P);
-    if (chunk > 65280) {  // u16 histogram exchange: per-rank counts must stay < 2^16
-      if (!grow()) return kFusedUnsupported;
-      continue;
+    const bool fits = chunk <= 65280  // u16 histogram exchange: per-rank counts must stay < 2^16
+                      && (L.total <= smem_cap || (stages == 2 && L.total <= (kCtasPerSm == 1 ? 220 : 108) * 1024));
+    if (fits) {
+      pl.ok = 1;
+      pl.qsplit = qsplit;
+      pl.G = G;
+      pl.C = C;
+      pl.P = P;
+      pl.chunk = (int)chunk;
+      pl.stages = stages;
+      pl.smem = L.total;
+      return pl;
     }
-    if (L.total <= smem_cap || (stages == 2 && L.total <= (kCtasPerSm == 1 ? 220 : 108) * 1024)) {
-      if (probe) return C;
-      FusedParams prm{};
-      prm.n_seqs = n_seqs;
-      prm.n_kv = n_kv;
-      prm.C = C;
-      prm.chunk = (int)chunk;
-      prm.budget = (int)budget;
-      prm.stages = stages;
-      prm.exact_encode = env_int("ADAMAS_EXACT_ENCODE", 0);
-      prm.dbg = env_int("ADAMAS_DBG", 0);
-      prm.pdl = env_int("ADAMAS_NO_PDL", 0) ? 0 : 1;
-      prm.append = append;
-      prm.qsplit = qsplit;
-      prm.P = P;
-      if (P > 1)
-        for (int i = 0; i < n_seqs; ++i)
-          if (int rc = ensure_unit_scratch(caches[i], (size_t)n_kv * qsplit * P * G)) return rc;
-      prm.cand = cand;
-      prm.cand_base = cand_base;
-      prm.peers = peers ? *peers : PeerPush{};
-      prm.q = q;
-      prm.k_new = k_new;
-      prm.v_new = v_new;
-      prm.out = out;
-      prm.idx = idx;
-      prm.status = caches[0]->status;
-      prm.trace = g_trace;
-      for (int i = 0; i < n_seqs; ++i) {
-        prm.seq[i].codes = caches[i]->codes;
-        prm.seq[i].K = caches[i]->K;
-        prm.seq[i].V = caches[i]->V;
-        prm.seq[i].cap = caches[i]->capacity;
-        prm.seq[i].s_old = caches[i]->seq_len;
-        prm.seq[i].clean = std::min(caches[i]->dirty_from, caches[i]->seq_len);
-        prm.seq[i].xhist = caches[i]->xhist;
-        prm.seq[i].xpart = caches[i]->xpart;
-        prm.seq[i].xsync = caches[i]->xsync;
-      }
-      return dtype == ADAMAS_BF16 ? launch_fused_dtype<__nv_bfloat16>(prm, G, C, L.total, s)
-                                  : launch_fused_dtype<float>(prm, G, C, L.total, s);
-    }
-    if (!grow()) return kFusedUnsupported;
+    if (C >= 16) return pl;  // out of options
+    C *= 2;
   }
+}
+
+// The automatic q-split: clusters above 4 CTAs do not reach a full wave of
+// co-resident CTAs on B200 (measured), so take the smallest split of a
+// kv-head's q-heads over clusters (each re-reads the codes) whose launch uses
+// C <= 4; with more than one wave of CTAs, splitting the q-heads beats
+// splitting the tokens at the same CTA count (measured: 16 x 32K Llama batch,
+// qsplit 1 x C 2 101 us vs qsplit 2 x C 1 87 us per layer-step).
+FusedPlan plan_fused(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, const Tuning& tu) {
+  if (qsplit > 0) return plan_for_split(n_seqs, n_kv, n_q, s_max, budget, qsplit, tu);
+  if (tu.qsplit > 0) return plan_for_split(n_seqs, n_kv, n_q, s_max, budget, tu.qsplit, tu);
+  const int G_all = n_q / n_kv;
+  FusedPlan best;
+  for (int qs = 1; qs <= G_all; qs *= 2) {
+    if (G_all % qs) break;
+    const FusedPlan pl = plan_for_split(n_seqs, n_kv, n_q, s_max, budget, qs, tu);
+    if (!pl.ok) continue;
+    if (pl.C <= 4) { best = pl; break; }
+    if (!best.ok || pl.C < best.C) best = pl;
+  }
+  if (best.ok && best.C > 1 && (int64_t)n_seqs * n_kv * best.qsplit * best.C > sm_count() &&
+      G_all % (2 * best.qsplit) == 0) {
+    const FusedPlan p2 = plan_for_split(n_seqs, n_kv, n_q, s_max, budget, 2 * best.qsplit, tu);
+    if (p2.ok && p2.C < best.C) best = p2;
+  }
+  return best;
+}
+
+// Plans are pure functions of the shape and the tuning: the last few are
+// cached (a decode loop repeats the same shape for every layer).
+FusedPlan plan_cached(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, const Tuning& tu) {
+  struct Entry {
+    int dev, n_seqs, n_kv, n_q, qsplit;
+    int64_t s_max, budget;
+    unsigned gen;
+    FusedPlan plan;
+  };
+  static std::mutex mu;
+  static Entry ring[16];
+  static int used = 0, next = 0;
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < used; ++i) {
+      const Entry& e = ring[i];
+      if (e.dev == dev && e.n_seqs == n_seqs && e.n_kv == n_kv && e.n_q == n_q && e.qsplit == qsplit &&
+          e.s_max == s_max && e.budget == budget && e.gen == tu.generation)
+        return e.plan;
+    }
+  }
+  const FusedPlan pl = plan_fused(n_seqs, n_kv, n_q, s_max, budget, qsplit, tu);
+  std::lock_guard<std::mutex> lock(mu);
+  ring[next] = Entry{dev, n_seqs, n_kv, n_q, qsplit, s_max, budget, tu.generation, pl};
+  next = (next + 1) % 16;
+  used = std::min(used + 1, 16);
+  return pl;
+}
+
+// Plans and launches one fused decode step. Returns kFusedUnsupported when
+// the shape does not fit the single-launch kernel (the caller composes
+// operators instead).
+int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n_q, int dtype, const void* q,
+                        const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
+                        cudaStream_t s, int append = 1, uint32_t* cand = nullptr, int64_t cand_base = 0,
+                        int qsplit = 0, const PeerPush* peers = nullptr) {
+  const Tuning tu = tuning();
+  int64_t s_max = 0;
+  for (int i = 0; i < n_seqs; ++i) s_max = std::max(s_max, caches[i]->seq_len + append);
+  if (s_max < 1) s_max = 1;
+  const FusedPlan pl = plan_cached(n_seqs, n_kv, n_q, s_max, budget, qsplit, tu);
+  if (!pl.ok) return kFusedUnsupported;
+  FusedParams prm{};
+  prm.n_seqs = n_seqs;
+  prm.n_kv = n_kv;
+  prm.C = pl.C;
+  prm.chunk = pl.chunk;
+  prm.budget = (int)budget;
+  prm.stages = pl.stages;
+  prm.exact_encode = tu.exact_encode;
+  prm.dbg = tu.dbg;
+  prm.pdl = tu.no_pdl ? 0 : 1;
+  prm.append = append;
+  prm.qsplit = pl.qsplit;
+  prm.P = pl.P;
+  if (pl.P > 1)
+    for (int i = 0; i < n_seqs; ++i)
+      if (int rc = ensure_unit_scratch(caches[i], (size_t)n_kv * pl.qsplit * pl.P * pl.G)) return rc;
+  prm.cand = cand;
+  prm.cand_base = cand_base;
+  prm.peers = peers ? *peers : PeerPush{};
+  prm.q = q;
+  prm.k_new = k_new;
+  prm.v_new = v_new;
+  prm.out = out;
+  prm.idx = idx;
+  prm.trace = g_trace;
+  for (int i = 0; i < n_seqs; ++i) {
+    prm.seq[i].codes = caches[i]->codes;
+    prm.seq[i].K = caches[i]->K;
+    prm.seq[i].V = caches[i]->V;
+    prm.seq[i].status = caches[i]->status;
+    prm.seq[i].cap = caches[i]->capacity;
+    prm.seq[i].s_old = caches[i]->seq_len;
+    prm.seq[i].clean = std::min(caches[i]->dirty_from, caches[i]->seq_len);
+    prm.seq[i].xhist = caches[i]->xhist;
+    prm.seq[i].xpart = caches[i]->xpart;
+    prm.seq[i].xsync = caches[i]->xsync;
+  }
+  return dtype == ADAMAS_BF16 ? launch_fused_dtype<__nv_bfloat16>(prm, pl.G, pl.C, pl.smem, s)
+                              : launch_fused_dtype<float>(prm, pl.G, pl.C, pl.smem, s);
 }
 
 }  // namespace
@@ -514,14 +612,19 @@ int pool_grow(void** p, size_t* have, size_t need, cudaStream_t s) {
 
 // dynamic shared memory of seq_select_attend_kernel: the q-head's keys
 size_t sel_smem(int n_ranks, int64_t budget) {
-  static const bool init = [] {  // up to kSelMaxKeys keys (32 KB) on top of ~29 KB static
+  // up to kSelMaxKeys keys (32 KB) on top of ~29 KB static; a function
+  // attribute is per device
+  static std::mutex mu;
+  static bool done[64] = {};
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
     cudaFuncSetAttribute(seq_select_attend_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSelMaxKeys * 4);
     cudaFuncSetAttribute(seq_select_attend_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSelMaxKeys * 4);
-    return true;
-  }();
-  (void)init;
+    done[dev] = true;
+  }
   return (size_t)n_ranks * budget * sizeof(uint32_t);
 }
 
@@ -539,8 +642,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool no_pdl = env_int("ADAMAS_NO_PDL", 0) != 0;
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  cfg.numAttrs = tuning().no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
@@ -575,6 +677,29 @@ int dot_scores(const double* q, const double* keys, int64_t n_rows, int64_t rows
 extern "C" {
 
 void adamas_debug_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
+
+int adamas_set_tuning(const int* values, int n) {
+  if (n < 0 || (n > 0 && !values)) return fail(ADAMAS_ERR_CONFIG, "set_tuning: bad arguments");
+  std::lock_guard<std::mutex> lock(g_tuning_mu);
+  Tuning& t = tuning_ref();
+  int* fields[] = {&t.qsplit, &t.cluster, &t.P, &t.stages, &t.smem_kb, &t.exact_encode, &t.dbg,
+                   &t.no_pdl, &t.composed, &t.require_fused};
+  constexpr int kFields = (int)(sizeof(fields) / sizeof(fields[0]));
+  if (n > kFields) return fail(ADAMAS_ERR_CONFIG, "set_tuning: too many values");
+  for (int i = 0; i < n; ++i) *fields[i] = values[i];
+  if (t.P < 1) t.P = 1;
+  ++t.generation;
+  return ADAMAS_OK;
+}
+
+int adamas_get_tuning(int* values, int n) {
+  if (n < 0 || (n > 0 && !values)) return fail(ADAMAS_ERR_CONFIG, "get_tuning: bad arguments");
+  const Tuning t = tuning();
+  const int v[] = {t.qsplit, t.cluster, t.P, t.stages, t.smem_kb, t.exact_encode, t.dbg, t.no_pdl, t.composed,
+                   t.require_fused};
+  for (int i = 0; i < n && i < (int)(sizeof(v) / sizeof(v[0])); ++i) values[i] = v[i];
+  return ADAMAS_OK;
+}
 
 const char* adamas_version(void) { return "adamas-b200 0.1 (sm_100a)"; }
 
@@ -736,10 +861,8 @@ int adamas_topk(const int32_t* scores, int n_rows, int64_t n, int64_t k, int32_t
   if (n_rows < 1 || n < 0 || k < 0) return fail(ADAMAS_ERR_CONFIG, "topk: bad sizes");
   if (k == 0) return ADAMAS_OK;
   if (!idx || (n > 0 && !scores)) return fail(ADAMAS_ERR_CONFIG, "topk: null pointer");
-  if (n > (int64_t(1) << 31) - 1) return fail(ADAMAS_ERR_CONFIG, "topk: n too large");
-  static int* dummy_status = nullptr;
-  if (!dummy_status) ADAMAS_CUDA(cudaMalloc(&dummy_status, sizeof(int)));
-  topk_kernel<<<n_rows, kTopkThreads, 0, as_stream(stream)>>>(scores, n, k, idx, dummy_status);
+  if (n > (int64_t(1) << 31) - 1 || k > (int64_t(1) << 31) - 1) return fail(ADAMAS_ERR_CONFIG, "topk: n or k too large");
+  topk_kernel<<<n_rows, kTopkThreads, 0, as_stream(stream)>>>(scores, n, k, idx);
   return launch_check("topk_kernel");
 }
 
@@ -752,11 +875,12 @@ int adamas_sparse_attention(const adamas_cache* c, const void* q, int n_q, const
   const int group = n_q / c->n_kv;
   if (c->dtype == ADAMAS_BF16)
     attend_kernel<__nv_bfloat16><<<n_q, kAttnWarps * 32, 0, as_stream(stream)>>>(
-        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, idx,
-        k, out, lse);
+        (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V, c->capacity, c->seq_len, group,
+        (const __nv_bfloat16*)q, idx, k, out, lse, c->status);
   else
     attend_kernel<float><<<n_q, kAttnWarps * 32, 0, as_stream(stream)>>>(
-        (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, idx, k, out, lse);
+        (const float*)c->K, (const float*)c->V, c->capacity, c->seq_len, group, (const float*)q, idx, k, out, lse,
+        c->status);
   return launch_check("attend_kernel");
 }
 
@@ -778,11 +902,12 @@ int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const vo
   }
   const size_t es = elem_size(c0->dtype);
   const size_t q_stride = (size_t)n_q * kHeadDim * es, kv_stride = (size_t)c0->n_kv * kHeadDim * es;
-  int rc = env_int("ADAMAS_NO_FUSED", 0)
+  const Tuning tu = tuning();
+  int rc = tu.composed
                ? kFusedUnsupported
                : fused_decode_launch(caches, n_seqs, c0->n_kv, n_q, c0->dtype, q, k_new, v_new, budget, out, idx,
                                      as_stream(stream));
-  if (rc == kFusedUnsupported && env_int("ADAMAS_REQUIRE_FUSED", 0))
+  if (rc == kFusedUnsupported && tu.require_fused)
     return fail(ADAMAS_ERR_CONFIG, "decode: shape not supported by the fused kernel (ADAMAS_REQUIRE_FUSED)");
   if (rc == kFusedUnsupported) {
     // Operator composition (same semantics, several launches).
@@ -1469,7 +1594,28 @@ int adamas_seq_step_p2p(adamas_cache* c, adamas_mailbox* m, const void* q, int n
                         int32_t* global_idx, void* stream) {
   if (!out) return fail(ADAMAS_ERR_CONFIG, "seq_step_p2p: null out");
   if (int rc = adamas_seq_p2p_local(c, m, q, n_q, k_new, v_new, append, base_index, stream)) return rc;
-  if (n_q <= sm_count())  // every select CTA resident: merge in the same launch
+  // merge in the same launch only when every select CTA is resident at once
+  // (its CTAs wait for each other's partials): occupancy, not just the SM count
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, int>, int>> resident;  // ((device, dtype) -> CTAs per SM)
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    const int dev = current_device();
+    for (auto& e : resident)
+      if (e.first.first == dev && e.first.second == c->dtype) per_sm = e.second;
+    if (per_sm == 0) {
+      const size_t dyn = sel_smem(m->world, m->budget);
+      cudaError_t e = c->dtype == ADAMAS_BF16
+                          ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seq_select_attend_kernel<__nv_bfloat16>,
+                                                                         kSelThreads, dyn)
+                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seq_select_attend_kernel<float>,
+                                                                         kSelThreads, dyn);
+      if (e != cudaSuccess || per_sm < 0) per_sm = 0;
+      resident.push_back({{dev, c->dtype}, per_sm});
+    }
+  }
+  if ((int64_t)n_q <= (int64_t)per_sm * sm_count())
     return p2p_select_attend(c, m, q, n_q, total_len, base_index, global_idx, out, stream);
   if (int rc = adamas_seq_p2p_select_attend(c, m, q, n_q, total_len, base_index, global_idx, stream)) return rc;
   return adamas_seq_p2p_merge(m, out, stream);

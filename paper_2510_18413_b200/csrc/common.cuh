@@ -30,6 +30,7 @@ constexpr double kQ28 = 0.6744897501960817432;
 constexpr int kStatusDegenerate = 1;  // zero or non-finite vector (quantizer.cpp:46-47)
 constexpr int kStatusSyncTimeout = 4;  // a multi-cluster unit barrier gave up (results invalid)
 constexpr int kStatusPeerTimeout = 8;  // a peer-memory exchange wait gave up (results invalid)
+constexpr int kStatusBadSelection = 16;  // gather indices not strictly increasing / out of range, or empty (kv_cache.cpp:90-91, attention.cpp:42)
 
 // ---------------------------------------------------------------- peer-memory exchange
 // Sequence-sharded decode exchanges its two small messages (the
@@ -56,6 +57,27 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Loads of mailbox memory that other GPUs (or other kernels still running)
+// write: coherent system-scope relaxed loads, never the read-only (.nc /
+// LDG.CONSTANT) path. Ordered after peer_wait's acquire by the CTA barrier
+// that follows it.
+__device__ __forceinline__ uint32_t ld_mailbox(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_mailbox(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_mailbox4(const float* p) {
+  float4 v;
+  asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
   return v;
 }
 

@@ -66,6 +66,7 @@ struct FusedSeq {
   int64_t cap;
   int64_t s_old;  // tokens in the cache before this step's append
   int64_t clean;  // tokens [0, clean) were not written by the preceding kernel: streamable before the PDL wait
+  int* status;    // this cache's sticky status word
   // multi-cluster units (FusedParams::P > 1): global scratch of this cache
   uint32_t* xhist;  // [unit][P][G][kHistBins] cluster-combined histograms
   float* xpart;     // [unit][P][G][kPartStride] cluster partials
@@ -88,7 +89,6 @@ struct FusedParams {
   const void* v_new;
   float* out;    // [n_seqs][n_q][128]
   int32_t* idx;  // [n_seqs][n_q][budget] or null
-  int* status;
   unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
   FusedSeq seq[kMaxSeqs];
 };
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       for (int w = 0; w < 4; ++w) { c.lo[w] = __float_as_uint(f[w]); c.hi[w] = 0u; }
       if (lane == 0) qcode[warp] = c;
     } else if (!encode128_to(f, sqs + warp * kHeadDim, qcode + warp, p.exact_encode != 0) && lane == 0) {
-      atomicOr(p.status, kStatusDegenerate);
+      atomicOr(p.seq[si].status, kStatusDegenerate);
     }
     ADAMAS_TRACE(13);
   } else if (has_new && warp == G) {  // append (kv_cache.cpp:62-71); part 0 of a split kv-head writes
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     float kf[4];
     Raw4<T>::to_float(kr, kf);
     if (!encode128_to(kf, sqs + G * kHeadDim, qcode + G, p.exact_encode != 0) && lane == 0)
-      atomicOr(p.status, kStatusDegenerate);
+      atomicOr(p.seq[si].status, kStatusDegenerate);
     if (lane == 0 && part == 0) store_code(planes, cap, s_old, qcode[G]);  // written by this lane
   }
   consumer_sync();
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         }
       }
       consumer_sync();
-      if (tid == 0) unit_barrier(p.seq[si].xsync + xunit * 4, P * owners, true, p.status);
+      if (tid == 0) unit_barrier(p.seq[si].xsync + xunit * 4, P * owners, true, p.seq[si].status);
       consumer_sync();
     }
     for (int j = 0; j < n_owned; ++j) {  // uniform within the CTA
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   }
   if (P > 1 && n_owned) {
     consumer_sync();
-    if (tid == 0) unit_barrier(p.seq[si].xsync + xunit * 4 + 2, P * owners, pc == 0, p.status);
+    if (tid == 0) unit_barrier(p.seq[si].xsync + xunit * 4 + 2, P * owners, pc == 0, p.seq[si].status);
     consumer_sync();
     if (pc == 0) {
       for (int g = warp; g < G; g += kConsumerWarps) {

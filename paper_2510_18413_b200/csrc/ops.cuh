@@ -218,13 +218,15 @@ score_kernel(const uint4* __restrict__ codes, int64_t cap, int64_t S, int group,
 }
 
 // ----------------------------------------------------------------- top_k
-// One CTA per row: histogram of the (small, non-negative) scores, threshold
-// T = smallest value whose cumulative count reaches k, then an order-preserving
-// compaction of {score < T} plus the first (k - #below) indices with score == T
-// (estimator.cpp:81-88: ties resolve toward the smaller index). The output is
-// ascending by construction; no sort.
+// One CTA per row: the k smallest int32 scores under the order (score, index)
+// (estimator.cpp:75-90: any int32, ties toward the smaller index), as ascending
+// indices. Radix select over order keys u = score ^ 0x80000000 (unsigned order =
+// signed order), 8-bit digits from the highest digit in which the row's min and
+// max keys differ (2-bit distances <= 384 take 2 passes, any int32 at most 4),
+// then an order-preserving compaction of {key < T} plus the first
+// (k - #below) indices with key == T. The output is ascending by construction;
+// no sort.
 constexpr int kTopkThreads = 1024;
-constexpr int kTopkBins = 1024;
 
 // Exclusive prefix of a 0/1 flag over the CTA in thread order; returns the
 // prefix and writes the CTA total to *total. `scratch` holds 32 ints.
@@ -245,12 +247,15 @@ __device__ __forceinline__ int block_flag_scan(bool flag, int* scratch, int* tot
   return before + in_warp;
 }
 
+__device__ __forceinline__ uint32_t topk_key(int32_t v) { return (uint32_t)v ^ 0x80000000u; }
+
 __global__ void __launch_bounds__(kTopkThreads)
-topk_kernel(const int32_t* __restrict__ scores, int64_t n, int64_t k, int32_t* __restrict__ idx,
-            int* __restrict__ status) {
-  __shared__ int hist[kTopkBins];
+topk_kernel(const int32_t* __restrict__ scores, int64_t n, int64_t k, int32_t* __restrict__ idx) {
+  __shared__ unsigned hist[256];
   __shared__ int scratch[32];
-  __shared__ int s_T, s_need;
+  __shared__ uint32_t s_min[32], s_max[32];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_need;
   const int row = blockIdx.x;
   const int32_t* s = scores + (int64_t)row * n;
   int32_t* out = idx + (int64_t)row * k;
@@ -261,56 +266,81 @@ topk_kernel(const int32_t* __restrict__ scores, int64_t n, int64_t k, int32_t* _
     return;
   }
   if (k == 0) return;
-  for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the row's key range: leading digits shared by every key need no pass
+  uint32_t lo = 0xffffffffu, hi = 0u;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    int v = s[i];
-    if (v < 0 || v >= kTopkBins) {
-      atomicOr(status, 2);
-      v = v < 0 ? 0 : kTopkBins - 1;
+    const uint32_t u = topk_key(s[i]);
+    lo = min(lo, u);
+    hi = max(hi, u);
+  }
+  lo = __reduce_min_sync(kFull, lo);
+  hi = __reduce_max_sync(kFull, hi);
+  if (lane == 0) { s_min[warp] = lo; s_max[warp] = hi; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    lo = __reduce_min_sync(kFull, lane < nw ? s_min[lane] : 0xffffffffu);
+    hi = __reduce_max_sync(kFull, lane < nw ? s_max[lane] : 0u);
+    if (lane == 0) {
+      s_min[0] = lo;
+      s_max[0] = hi;
+      s_need = (int)k;
     }
-    atomicAdd(&hist[v], 1);
   }
   __syncthreads();
-  // inclusive scan of the histogram (one bin per thread)
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int v = hist[threadIdx.x];
-#pragma unroll
-    for (int m = 1; m < 32; m <<= 1) {
-      const int o = __shfl_up_sync(kFull, v, m);
-      if (lane >= m) v += o;
-    }
-    if (lane == 31) scratch[warp] = v;
+  lo = s_min[0];
+  hi = s_max[0];
+  const uint32_t diff = lo ^ hi;
+  int shift = diff ? ((31 - __clz(diff)) / 8) * 8 : -8;  // top digit in which keys differ
+  if (threadIdx.x == 0) s_prefix = shift + 8 >= 32 ? 0u : (lo & (0xffffffffu << (shift + 8)));
+  __syncthreads();
+  for (; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    if (warp == 0) {
-      int w = scratch[lane];
+    const uint32_t prefix = s_prefix;
+    const uint32_t hi_mask = shift + 8 >= 32 ? 0u : (0xffffffffu << (shift + 8));
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t u = topk_key(s[i]);
+      if ((u & hi_mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {  // digit whose cumulative count reaches the remaining need
+      unsigned c[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[lane * 8 + j];
+        sum += c[j];
+      }
+      unsigned incl = sum;
 #pragma unroll
       for (int m = 1; m < 32; m <<= 1) {
-        const int o = __shfl_up_sync(kFull, w, m);
-        if (lane >= m) w += o;
+        const unsigned o = __shfl_up_sync(kFull, incl, m);
+        if (lane >= m) incl += o;
       }
-      scratch[lane] = w;
-    }
-    __syncthreads();
-    const int cum = v + (warp > 0 ? scratch[warp - 1] : 0);
-    const int prev = cum - hist[threadIdx.x];
-    if (prev < k && cum >= k) {
-      s_T = threadIdx.x;
-      s_need = (int)(k - prev);
+      const int need = s_need;
+      unsigned before = incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if ((int)before < need && (int)(before + c[j]) >= need) {
+          s_prefix = prefix | ((uint32_t)(lane * 8 + j) << shift);
+          s_need = need - (int)before;
+        }
+        before += c[j];
+      }
     }
     __syncthreads();
   }
-  const int T = s_T;
-  const int need = s_need;
+  const uint32_t T = s_prefix;
+  const int need = s_need;  // keys equal to T to take, in index order
   int eq_seen = 0, taken = 0;
   for (int64_t base = 0; base < n; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    const int v = i < n ? s[i] : 0x7fffffff;
-    const bool eq = (i < n) && v == T;
+    const uint32_t u = i < n ? topk_key(s[i]) : 0xffffffffu;
+    const bool eq = (i < n) && u == T;
     int eq_total;
     const int eq_before = eq_seen + block_flag_scan(eq, scratch, &eq_total);
-    const bool take = (i < n) && (v < T || (eq && eq_before < need));
+    const bool take = (i < n) && (u < T || (eq && eq_before < need));
     int take_total;
     const int pos = taken + block_flag_scan(take, scratch, &take_total);
     if (take) out[pos] = (int32_t)i;
@@ -328,13 +358,33 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 template <typename T>
 __global__ void __launch_bounds__(kAttnWarps * 32)
-attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
+attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int64_t seq_len, int group,
               const T* __restrict__ q, const int32_t* __restrict__ idx, int64_t k,
-              float* __restrict__ out, float* __restrict__ lse) {
+              float* __restrict__ out, float* __restrict__ lse, int* __restrict__ status) {
   __shared__ float sm[kAttnWarps], sl[kAttnWarps];
   __shared__ float so[kAttnWarps][kHeadDim];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hq = blockIdx.x, hk = hq / group;
+  {  // KvCache::gather preconditions (kv_cache.cpp:90-91) and the empty selection
+     // (attention.cpp:42): a row is a strictly increasing run of indices in
+     // [0, seq_len), optionally followed by -1 entries only. A bad row latches
+     // kStatusBadSelection and reads nothing.
+    const int32_t* row = idx + (int64_t)hq * k;
+    bool bad = false;
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+      const int32_t t = row[i], prev = i > 0 ? row[i - 1] : -1;
+      if (t >= 0) bad |= t >= seq_len || (i > 0 && prev < 0) || (i > 0 && prev >= t);
+      else bad |= t != -1 || i == 0;
+    }
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) atomicOr(status, kStatusBadSelection);
+      if (warp == 0) {
+        *reinterpret_cast<float4*>(out + (int64_t)hq * kHeadDim + lane * 4) = make_float4(NAN, NAN, NAN, NAN);
+        if (lse != nullptr && lane == 0) { lse[2 * hq] = NAN; lse[2 * hq + 1] = 0.f; }
+      }
+      return;
+    }
+  }
   float qf[4];
   Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)hq * kHeadDim + lane * 4), qf);
   // logits in log2 units: q.k / sqrt(128) * log2(e)
@@ -427,11 +477,11 @@ __device__ __forceinline__ void sel_block_excl_scan(int v, int& excl, int& total
 template <typename T>
 __global__ void __launch_bounds__(kSelThreads)
 seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
-                         const T* __restrict__ q, const uint32_t* __restrict__ keys, int n_ranks, int n_q,
+                         const T* __restrict__ q, const uint32_t* keys, int n_ranks, int n_q,
                          int64_t budget, int k_eff, int64_t rank_base, int64_t rank_len, float* __restrict__ partial,
                          int32_t* __restrict__ gidx, const __grid_constant__ PeerPush push,
-                         const uint32_t* __restrict__ wait_flags, int* __restrict__ status,
-                         const float* __restrict__ merge_parts, const uint32_t* __restrict__ merge_flags,
+                         const uint32_t* wait_flags, int* __restrict__ status,
+                         const float* merge_parts, const uint32_t* merge_flags,
                          float* __restrict__ merge_out) {
   extern __shared__ uint32_t skeys[];  // the n_ranks * budget keys of this q-head, read once
   __shared__ int hist[kSelBins];
@@ -461,7 +511,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   __syncthreads();
   for (int j = tid; j < n; j += kSelThreads) {
     const int r = j / (int)budget, i = j - r * (int)budget;
-    const uint32_t key = keys[((int64_t)r * n_q + h) * budget + i];
+    const uint32_t key = ld_mailbox(keys + ((int64_t)r * n_q + h) * budget + i);
     skeys[j] = key;
     if (key != 0xffffffffu) atomicAdd(&hist[key >> 23], 1);
   }
@@ -588,15 +638,16 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
       float M = -INFINITY;
       for (int r = 0; r < n_ranks; ++r) {
         const float* pp = merge_parts + ((int64_t)r * n_q + h) * kPartialStride;
-        if (pp[1] > 0.f) M = fmaxf(M, pp[0]);
+        if (ld_mailbox(pp + 1) > 0.f) M = fmaxf(M, ld_mailbox(pp));
       }
       float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
       for (int r = 0; r < n_ranks; ++r) {
         const float* pp = merge_parts + ((int64_t)r * n_q + h) * kPartialStride;
-        if (!(pp[1] > 0.f)) continue;
-        const float c = __expf(pp[0] - M);
-        L += pp[1] * c;
-        const float4 v = *reinterpret_cast<const float4*>(pp + 4 + lane * 4);
+        const float lr = ld_mailbox(pp + 1);
+        if (!(lr > 0.f)) continue;
+        const float c = __expf(ld_mailbox(pp) - M);
+        L += lr * c;
+        const float4 v = ld_mailbox4(pp + 4 + lane * 4);
         acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
       }
       const float inv = L > 0.f ? 1.f / L : 0.f;
@@ -608,9 +659,8 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
 
 // out[h] = sum_r e^{m_r - M} o_r / sum_r e^{m_r - M} l_r over the ranks' partials.
 // With wait_flags, first acquires every rank's partial epoch (peer exchange).
-__global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks, int n_q, float* __restrict__ out,
-                                 const uint32_t* __restrict__ wait_flags, const uint32_t* __restrict__ epoch,
-                                 int* __restrict__ status) {
+__global__ void lse_merge_kernel(const float* partials, int n_ranks, int n_q, float* __restrict__ out,
+                                 const uint32_t* wait_flags, const uint32_t* epoch, int* __restrict__ status) {
   const int h = blockIdx.x, lane = threadIdx.x;
   grid_dependency_wait();  // partials come from the preceding kernel (PDL launch)
   if (lane == 0) grid_launch_dependents();
@@ -621,15 +671,16 @@ __global__ void lse_merge_kernel(const float* __restrict__ partials, int n_ranks
   float M = -INFINITY;
   for (int r = 0; r < n_ranks; ++r) {
     const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
-    if (pp[1] > 0.f) M = fmaxf(M, pp[0]);
+    if (ld_mailbox(pp + 1) > 0.f) M = fmaxf(M, ld_mailbox(pp));
   }
   float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int r = 0; r < n_ranks; ++r) {
     const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
-    if (!(pp[1] > 0.f)) continue;
-    const float c = __expf(pp[0] - M);
-    L += pp[1] * c;
-    const float4 v = *reinterpret_cast<const float4*>(pp + 4 + lane * 4);
+    const float lr = ld_mailbox(pp + 1);
+    if (!(lr > 0.f)) continue;
+    const float c = __expf(ld_mailbox(pp) - M);
+    L += lr * c;
+    const float4 v = ld_mailbox4(pp + 4 + lane * 4);
     acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;

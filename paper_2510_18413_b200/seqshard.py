@@ -32,7 +32,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import check, load
+from ._lib import ADAMAS_STATUS_PEER_TIMEOUT, AdamasRuntimeError, check, load
 
 HEAD_DIM = 128
 PARTIAL_STRIDE = 132
@@ -143,11 +143,14 @@ class SeqShardedDecoder:
         check(self.ops.L.adamas_seq_p2p_merge(mailbox.h, _ptr(out), _stream(stream)))
         return out
 
-    def decode_step_p2p(self, mailbox: Mailbox, q, k_new, v_new, want_idx=False, stream=None):
+    def decode_step_p2p(self, mailbox: Mailbox, q, k_new, v_new, want_idx=False, check_status=True, stream=None):
         """One step over peer memory (every rank calls it; no collective call):
         adamas_seq_step_p2p, whose select/attend launch also does the merge.
         Ranks must run concurrently (one per GPU / process); ranks simulated
-        in one stream use simulate_step_p2p's phase-by-phase order instead."""
+        in one stream use simulate_step_p2p's phase-by-phase order instead.
+        check_status (default) synchronizes and raises if a peer wait timed
+        out (the outputs of such a step are invalid); a tight loop may pass
+        False and call mailbox.raise_on_timeout() periodically instead."""
         append = self.rank == self.tail
         n_q = q.numel() // HEAD_DIM
         out = torch.empty((n_q, HEAD_DIM), dtype=torch.float32, device=q.device)
@@ -157,6 +160,8 @@ class SeqShardedDecoder:
                                              _ptr(v_new if append else None), int(append), self.base, total,
                                              _ptr(out), _ptr(gidx), _stream(stream)))
         self.lengths[self.tail] += 1
+        if check_status:
+            mailbox.raise_on_timeout()
         return out, gidx
 
     def decode_step(self, q, k_new, v_new, budget: int, allgather, want_idx=False):
@@ -200,6 +205,14 @@ class Mailbox:
         check(self.L.adamas_mailbox_status(self.h, C.byref(v)))
         return v.value
 
+    def raise_on_timeout(self) -> None:
+        """A peer wait that gave up (ADAMAS_STATUS_PEER_TIMEOUT) means this
+        step read stale keys / partials: its outputs are invalid."""
+        st = self.status()
+        if st & ADAMAS_STATUS_PEER_TIMEOUT:
+            raise AdamasRuntimeError(f"peer-memory exchange timed out on rank {self.rank} (status {st:#x}); "
+                                     "the step's outputs are invalid")
+
     def close(self):
         if self.h:
             self.L.adamas_mailbox_destroy(self.h)
@@ -230,12 +243,15 @@ def torch_allgather(group=None):
     return gather
 
 
-def simulate_step_p2p(decoders, mailboxes, qs, k_new, v_new, want_idx=False):
+def simulate_step_p2p(decoders, mailboxes, qs, k_new, v_new, want_idx=False, check_status=True):
     """All ranks of one process over locally connected mailboxes, phase by phase."""
     for d, m, q in zip(decoders, mailboxes, qs):
         d.local_p2p(m, q, k_new, v_new)
     gidx = [d.attend_p2p(m, q, want_idx) for d, m, q in zip(decoders, mailboxes, qs)]
     outs = [d.merge_p2p(m) for d, m in zip(decoders, mailboxes)]
+    if check_status:
+        for m in mailboxes:
+            m.raise_on_timeout()
     return outs, gidx
 
 

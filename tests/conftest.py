@@ -41,3 +41,12 @@ def gpu():
         pytest.fail("GPU test selected but no CUDA device is visible")
     import paper_2510_18413_b200 as ad
     return ad
+
+
+@pytest.fixture
+def tune(gpu):
+    """tune(cluster=4, qsplit=2, ...): launch-plan overrides through the C ABI
+    (adamas_set_tuning), restored after the test."""
+    saved = gpu.get_tuning()
+    yield lambda **kw: gpu.set_tuning(**kw)
+    gpu.set_tuning(**saved)

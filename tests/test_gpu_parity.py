@@ -163,41 +163,41 @@ def test_fused_decode_multi_step(gpu, oracle):
 
 
 @pytest.mark.parametrize("cluster", ["1", "2", "8", "16"])
-def test_fused_decode_cluster_sizes(gpu, oracle, monkeypatch, cluster):
-    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+def test_fused_decode_cluster_sizes(gpu, oracle, tune, cluster):
+    tune(cluster=int(cluster))
     run_decode(gpu, oracle, 6000, 2, 1, 128, True, seed=int(cluster))
 
 
 @pytest.mark.parametrize("qsplit", ["1", "2", "4"])
-def test_fused_decode_qsplit(gpu, oracle, monkeypatch, qsplit):
+def test_fused_decode_qsplit(gpu, oracle, tune, qsplit):
     """a kv-head's q-heads split over several clusters (each scans the codes
     for its share); the appended row comes from the input for every part"""
-    monkeypatch.setenv("ADAMAS_QSPLIT", qsplit)
+    tune(qsplit=int(qsplit))
     run_decode(gpu, oracle, 9000, 2, 4, 128, True, seed=71 + int(qsplit), steps=3)
 
 
 @pytest.mark.parametrize("cluster,G", [("2", 4), ("4", 4), ("2", 8)])
-def test_fused_decode_exchange_topologies(gpu, oracle, monkeypatch, cluster, G):
+def test_fused_decode_exchange_topologies(gpu, oracle, tune, cluster, G):
     """one-hop (C x G <= 8) and two-hop (C x G > 8) histogram exchanges,
     including owners of several heads (G > C)"""
-    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    tune(cluster=int(cluster))
     run_decode(gpu, oracle, 5000, 1, G, 96, True, seed=31 * G + int(cluster), steps=2)
 
 
 @pytest.mark.parametrize("S,G", [(8000, 1), (16000, 1), (32000, 1), (40000, 1),
                                  (70000, 1), (2000, 4), (4000, 4), (8000, 4), (9000, 4), (20000, 4)])
-def test_fused_compaction_span_sizes(gpu, oracle, monkeypatch, S, G):
+def test_fused_compaction_span_sizes(gpu, oracle, tune, S, G):
     """one CTA per unit, so the rank length picks the compaction instance:
     16..64-token spans (SW 2), 128-token spans (SW 4), or 32-token groups (SW 0)"""
-    monkeypatch.setenv("ADAMAS_CLUSTER", "1")
+    tune(cluster=1)
     run_decode(gpu, oracle, S, 1, G, 128, True, seed=S + 13 * G, steps=2)
 
 
 @pytest.mark.parametrize("cluster", ["1", "4"])
-def test_fused_decode_heavy_ties(gpu, oracle, monkeypatch, cluster):
+def test_fused_decode_heavy_ties(gpu, oracle, tune, cluster):
     """keys drawn from 6 distinct vectors: whole bins of equal distances at T,
     ties taken in index order across spans and ranks (estimator.cpp:75-90)"""
-    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    tune(cluster=int(cluster))
     S, n_kv, G, budget = 6001, 1, 2, 100
     K, V, q = make_inputs(S, n_kv, n_kv * G, True, 4242)
     pick = np.random.default_rng(7).integers(0, 6, S)
@@ -209,8 +209,8 @@ def test_fused_decode_heavy_ties(gpu, oracle, monkeypatch, cluster):
     assert rel_err(out.cpu().numpy(), eout).max() <= TOL[True]
 
 
-def test_operator_composition_matches_fused(gpu, oracle, monkeypatch):
-    monkeypatch.setenv("ADAMAS_NO_FUSED", "1")
+def test_operator_composition_matches_fused(gpu, oracle, tune):
+    tune(composed=1)
     run_decode(gpu, oracle, 2000, 2, 2, 64, False, seed=5, steps=2)
 
 
@@ -247,10 +247,10 @@ def test_cuda_path_reproduces_reference_golden(gpu, golden, name):
     assert rel_err(out.cpu().numpy(), golden[f"{name}/out"]).max() <= TOL[bool(bf16)]
 
 
-def test_fused_decode_exact_encode_path(gpu, oracle, monkeypatch):
+def test_fused_decode_exact_encode_path(gpu, oracle, tune):
     """The fused kernel's low-latency sigma (shuffle-tree sum with a near-tie
     guard) and the sequential-sum path give identical codes and selections."""
-    monkeypatch.setenv("ADAMAS_EXACT_ENCODE", "1")
+    tune(exact_encode=1)
     run_decode(gpu, oracle, 3000, 2, 4, 64, True, seed=31, steps=3)
 
 
@@ -280,11 +280,11 @@ def test_fast_encode_near_ties_and_scales(gpu, oracle):
 
 
 @pytest.mark.parametrize("cluster", ["1", "4"])
-def test_uncertified_appended_key(gpu, oracle, monkeypatch, cluster):
+def test_uncertified_appended_key(gpu, oracle, tune, cluster):
     """Appended keys built to sit on the +/- kQ28 sigma thresholds (the fp32
     certificate fails): the fused step takes the exact code (at G = 1 from the
     helper warp, after the scan), stores it in the cache and selects with it."""
-    monkeypatch.setenv("ADAMAS_CLUSTER", cluster)
+    tune(cluster=int(cluster))
     rng = np.random.default_rng(9)
     S, budget = 3000, 64
     K, V, q = make_inputs(S, 1, 1, False, 43)
@@ -371,18 +371,15 @@ def test_seq_shard_empty_rank_and_errors(gpu, oracle):
 
 
 @pytest.mark.parametrize("P,C,n_kv,G,steps", [(2, 4, 1, 1, 3), (4, 4, 2, 4, 2), (4, 2, 1, 2, 2), (8, 4, 1, 8, 1)])
-def test_fused_decode_multi_cluster_units(gpu, oracle, monkeypatch, P, C, n_kv, G, steps):
+def test_fused_decode_multi_cluster_units(gpu, oracle, tune, P, C, n_kv, G, steps):
     """A unit spanning P clusters: histograms and partials through global
     memory with the self-resetting barrier (reused across consecutive steps)."""
-    monkeypatch.setenv("ADAMAS_P", str(P))
-    monkeypatch.setenv("ADAMAS_CLUSTER", str(C))
-    monkeypatch.setenv("ADAMAS_REQUIRE_FUSED", "1")
+    tune(P=P, cluster=C, require_fused=1)
     cache = run_decode(gpu, oracle, 12000, n_kv, G, 128, True, seed=P * 10 + G, steps=steps)
     assert cache.status() == 0  # no barrier timeout
 
 
-def test_seq_shard_candidates_multi_cluster(gpu, oracle, monkeypatch):
-    monkeypatch.setenv("ADAMAS_P", "4")
-    monkeypatch.setenv("ADAMAS_CLUSTER", "4")
+def test_seq_shard_candidates_multi_cluster(gpu, oracle, tune):
+    tune(P=4, cluster=4)
     from tests.test_gpu_seqshard import test_seq_sharded_decode_matches_single_device as t
     t(gpu, oracle, 20000, 2, 2, 4, 128, True)

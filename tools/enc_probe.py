@@ -17,7 +17,7 @@ for _ in range(8):
 q = torch.randn((32, 128), generator=gen, device="cuda").bfloat16()
 trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
 for dbg in (32 | (13 << 8), 32 | (14 << 8), (13 << 8), (14 << 8)):
-    os.environ["ADAMAS_DBG"] = str(dbg)
+    ad.set_tuning(dbg=dbg)
     res = []
     for st in (12, 13):
         pass

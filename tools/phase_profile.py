@@ -75,7 +75,7 @@ def run_layers():
 
 
 def timed_graph(stamp):
-    os.environ["ADAMAS_DBG"] = str(base_dbg | ((stamp + 1) << 8 if stamp >= 0 else 0))
+    ad.set_tuning(dbg=base_dbg | ((stamp + 1) << 8 if stamp >= 0 else 0))
     trace.zero_()
     run_layers()
     torch.cuda.synchronize()
@@ -116,4 +116,4 @@ for i in (12, 13):
     us_i, ti = timed_graph(i)
     cum = (ti[:, i] - ti[:, 14]) / 1000.0
     print(f"stamp {i}: cum mean {cum.mean():.2f} max {cum.max():.2f}")
-os.environ["ADAMAS_DBG"] = str(base_dbg)
+ad.set_tuning(dbg=base_dbg)
