@@ -32,7 +32,9 @@ def _worker(rank, world, port, S, n_kv, G, budget, steps, seed):
         spec = importlib.util.spec_from_file_location(
             "seqshard_proto", os.path.join(root, "paper_2510_18413_b200", "seqshard.py"),
             submodule_search_locations=None)
-        src = open(spec.origin).read().replace("from ._lib import check, load", "check = load = None")
+        import re
+        src = re.sub(r"^from \._lib import .*$", "check = load = None\nADAMAS_STATUS_PEER_TIMEOUT = 8\n"
+                     "AdamasRuntimeError = RuntimeError", open(spec.origin).read(), flags=re.M)
         proto = type(sys)("seqshard_proto")
         exec(compile(src, spec.origin, "exec"), proto.__dict__)
 
