@@ -422,15 +422,6 @@ def run_ours(args):
                 parity = {"status": "MISMATCH", "detail": f"on rank {int(bad[0]) - 1}"}
             elif parity["status"] == "ok":
                 parity["checked"] += f"; every one of the {ws} ranks checked its own heads"
-    spec = None
-    if not seqshard:  # the speculative-threshold selection: listed path vs full-row fallback, all layers
-        tot = [0, 0]
-        for row in caches:
-            for c in row:
-                a_, b_ = c.spec_stats()
-                tot[0] += a_
-                tot[1] += b_
-        spec = {"listed_unit_steps": tot[0], "fallback_unit_steps": tot[1]}
     launches_per_step = L * (3 if seqshard else 1)
     ms_per_step = elapsed_ms / args.steps
     tokens_per_layer = NS  # one decoded token per sequence per layer
@@ -553,7 +544,6 @@ def run_ours(args):
             "clocks": clocks,
             "cpu_baseline": cpu,
             "parity": parity,
-            "speculative_select": spec,
         }
         print(json.dumps(line))
         if parity and parity["status"] != "ok":

@@ -77,10 +77,6 @@ int adamas_cache_truncate(adamas_cache* cache, int64_t seq_len);
 int adamas_cache_buffers(const adamas_cache* cache, void** keys, void** values, void** codes);
 /* Reads and clears the sticky device status word (synchronizes the stream). */
 int adamas_cache_status(adamas_cache* cache, void* stream, int* status);
-/* Counters of the decode step's speculative-threshold selection, per
- * (kv-head unit, step): how many took the listed path and how many fell back
- * to the full-row selection (both exact; synchronizes the stream). */
-int adamas_cache_spec_stats(adamas_cache* cache, void* stream, int64_t* listed, int64_t* fallback);
 
 /* Fused encode + append. Replaces, for every token and kv-head,
  * KvCache::update(k, v, pack(encode(k))) (kv_cache.cpp:62-71 with
@@ -331,13 +327,11 @@ void adamas_debug_trace(unsigned long long* device_buffer);
  * CTAs (0 auto), clusters per unit P (1), ring stages (0 auto), shared-memory
  * cap in KB (0 auto), exact fp64 encode (0), diagnostics switches (0), no PDL
  * (0), composed operators instead of the fused launch (0), require the fused
- * launch (0), speculative-threshold margin (6; negative = off: every step
- * takes the full-row selection). The initial values are read once from the
- * ADAMAS_QSPLIT, ADAMAS_CLUSTER, ADAMAS_P, ADAMAS_STAGES, ADAMAS_SMEM_KB,
- * ADAMAS_EXACT_ENCODE, ADAMAS_DBG, ADAMAS_NO_PDL, ADAMAS_NO_FUSED,
- * ADAMAS_REQUIRE_FUSED, ADAMAS_SPEC_MARGIN environment variables at first
- * use; nothing on the launch path reads the environment. */
-#define ADAMAS_TUNING_FIELDS 11
+ * launch (0). The initial values are read once from the ADAMAS_QSPLIT,
+ * ADAMAS_CLUSTER, ADAMAS_P, ADAMAS_STAGES, ADAMAS_SMEM_KB, ADAMAS_EXACT_ENCODE,
+ * ADAMAS_DBG, ADAMAS_NO_PDL, ADAMAS_NO_FUSED, ADAMAS_REQUIRE_FUSED environment
+ * variables at first use; nothing on the launch path reads the environment. */
+#define ADAMAS_TUNING_FIELDS 10
 int adamas_set_tuning(const int* values, int n);
 int adamas_get_tuning(int* values, int n);
 

@@ -20,7 +20,7 @@ ADAMAS_STATUS_SYNC_TIMEOUT = 4
 ADAMAS_STATUS_PEER_TIMEOUT = 8
 ADAMAS_STATUS_BAD_SELECTION = 16
 TUNING_FIELDS = ("qsplit", "cluster", "P", "stages", "smem_kb", "exact_encode", "dbg", "no_pdl", "composed",
-                 "require_fused", "spec_margin")
+                 "require_fused")
 
 EXPORTED = [
     "adamas_version", "adamas_last_error", "adamas_cache_create", "adamas_cache_destroy",
@@ -36,7 +36,7 @@ EXPORTED = [
     "adamas_pages_build", "adamas_pages_select", "adamas_mailbox_create", "adamas_mailbox_ipc_handle",
     "adamas_mailbox_connect", "adamas_mailbox_connect_local", "adamas_mailbox_status", "adamas_mailbox_destroy",
     "adamas_seq_p2p_local", "adamas_seq_p2p_select_attend", "adamas_seq_p2p_merge", "adamas_seq_step_p2p",
-    "adamas_set_tuning", "adamas_get_tuning", "adamas_cache_spec_stats",
+    "adamas_set_tuning", "adamas_get_tuning",
 ]
 
 
@@ -108,7 +108,6 @@ def load() -> C.CDLL:
     L.adamas_seq_step_p2p.argtypes = [vp, vp, vp, i32, vp, vp, i32, i64, i64, vp, vp, vp]
     L.adamas_topk_f64.argtypes = [vp, i64, i64, i64, vp, vp]
     L.adamas_set_tuning.argtypes = [C.POINTER(i32), i32]
-    L.adamas_cache_spec_stats.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64)]
     L.adamas_get_tuning.argtypes = [C.POINTER(i32), i32]
     L.adamas_page_select.argtypes = [vp, vp, i64, i64, i64, i64, i32, i64, i64, vp, vp, vp]
     L.adamas_attention_f64.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp, vp]

@@ -120,13 +120,6 @@ class KvCache:
         check(self.L.adamas_cache_status(self.h, _stream(stream), C.byref(s)))
         return s.value
 
-    def spec_stats(self, stream=None) -> tuple[int, int]:
-        """(listed, fallback): decode-step units that took the speculative
-        listed selection / fell back to the full-row selection (both exact)."""
-        a, b = C.c_int64(), C.c_int64()
-        check(self.L.adamas_cache_spec_stats(self.h, _stream(stream), C.byref(a), C.byref(b)))
-        return a.value, b.value
-
     def raise_on_status(self, stream=None) -> None:
         """Reads and clears the sticky status word; raises what the reference
         would have thrown: ConfigError for a zero / non-finite vector

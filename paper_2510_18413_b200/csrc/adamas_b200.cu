@@ -31,7 +31,6 @@ struct adamas_cache {
   void* V = nullptr;
   uint4* codes = nullptr;  // [n_kv][2 planes][capacity] x 16 B
   int* status = nullptr;  // device sticky status word
-  int* tprev = nullptr;   // [n_kv][kMaxTprevGroup] previous decode step's threshold per q-head (-1 unknown)
   // multi-cluster units: [unit][4] barrier words (zeroed once), lazily sized
   // histogram / partial scratch
   int* xsync = nullptr;
@@ -156,7 +155,6 @@ int env_int(const char* name, int dflt) {
 struct Tuning {
   int qsplit = 0, cluster = 0, P = 1, stages = 0, smem_kb = 0;
   int exact_encode = 0, dbg = 0, no_pdl = 0, composed = 0, require_fused = 0;
-  int spec_margin = 6;  // speculative threshold Tg = previous T + margin (< 0: off)
   unsigned generation = 0;  // bumped on every change: invalidates cached plans
 };
 std::mutex g_tuning_mu;
@@ -173,7 +171,6 @@ Tuning& tuning_ref() {
     x.no_pdl = env_int("ADAMAS_NO_PDL", 0);
     x.composed = env_int("ADAMAS_NO_FUSED", 0);
     x.require_fused = env_int("ADAMAS_REQUIRE_FUSED", 0);
-    x.spec_margin = env_int("ADAMAS_SPEC_MARGIN", 6);
     return x;
   }();
   return t;
@@ -436,7 +433,6 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
   prm.append = append;
   prm.qsplit = pl.qsplit;
   prm.P = pl.P;
-  prm.spec_margin = tu.spec_margin;
   if (pl.P > 1)
     for (int i = 0; i < n_seqs; ++i)
       if (int rc = ensure_unit_scratch(caches[i], (size_t)n_kv * pl.qsplit * pl.P * pl.G)) return rc;
@@ -454,7 +450,6 @@ int fused_decode_launch(adamas_cache* const* caches, int n_seqs, int n_kv, int n
     prm.seq[i].K = caches[i]->K;
     prm.seq[i].V = caches[i]->V;
     prm.seq[i].status = caches[i]->status;
-    prm.seq[i].tprev = n_q / n_kv <= kMaxTprevGroup ? caches[i]->tprev : nullptr;
     prm.seq[i].cap = caches[i]->capacity;
     prm.seq[i].s_old = caches[i]->seq_len;
     prm.seq[i].clean = std::min(caches[i]->dirty_from, caches[i]->seq_len);
@@ -688,7 +683,7 @@ int adamas_set_tuning(const int* values, int n) {
   std::lock_guard<std::mutex> lock(g_tuning_mu);
   Tuning& t = tuning_ref();
   int* fields[] = {&t.qsplit, &t.cluster, &t.P, &t.stages, &t.smem_kb, &t.exact_encode, &t.dbg,
-                   &t.no_pdl, &t.composed, &t.require_fused, &t.spec_margin};
+                   &t.no_pdl, &t.composed, &t.require_fused};
   constexpr int kFields = (int)(sizeof(fields) / sizeof(fields[0]));
   if (n > kFields) return fail(ADAMAS_ERR_CONFIG, "set_tuning: too many values");
   for (int i = 0; i < n; ++i) *fields[i] = values[i];
@@ -701,7 +696,7 @@ int adamas_get_tuning(int* values, int n) {
   if (n < 0 || (n > 0 && !values)) return fail(ADAMAS_ERR_CONFIG, "get_tuning: bad arguments");
   const Tuning t = tuning();
   const int v[] = {t.qsplit, t.cluster, t.P, t.stages, t.smem_kb, t.exact_encode, t.dbg, t.no_pdl, t.composed,
-                   t.require_fused, t.spec_margin};
+                   t.require_fused};
   for (int i = 0; i < n && i < (int)(sizeof(v) / sizeof(v[0])); ++i) values[i] = v[i];
   return ADAMAS_OK;
 }
@@ -737,12 +732,6 @@ int adamas_cache_create(adamas_cache** out, int n_kv_heads, int head_dim, int bi
   if (e == cudaSuccess) e = cudaMalloc(&c->codes, rows * 2 * sizeof(uint4));
   if (e == cudaSuccess) e = cudaMalloc(&c->status, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->status, 0, sizeof(int));
-  // previous thresholds [n_kv][kMaxTprevGroup] (-1: unknown), then two u64 counters of
-  // the speculative path (listed, fallback)
-  const size_t tp_bytes = (size_t)n_kv_heads * kMaxTprevGroup * sizeof(int);
-  if (e == cudaSuccess) e = cudaMalloc(&c->tprev, tp_bytes + 2 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(c->tprev, 0xff, tp_bytes);
-  if (e == cudaSuccess) e = cudaMemset(reinterpret_cast<char*>(c->tprev) + tp_bytes, 0, 2 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->xsync, (size_t)n_kv_heads * kMaxG * 4 * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->xsync, 0, (size_t)n_kv_heads * kMaxG * 4 * sizeof(int));
   if (e != cudaSuccess) {
@@ -759,7 +748,6 @@ int adamas_cache_destroy(adamas_cache* c) {
   cudaFree(c->V);
   cudaFree(c->codes);
   cudaFree(c->status);
-  cudaFree(c->tprev);
   cudaFree(c->xsync);
   cudaFree(c->xhist);
   cudaFree(c->xpart);
@@ -799,17 +787,6 @@ int adamas_cache_status(adamas_cache* c, void* stream, int* status) {
   ADAMAS_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), as_stream(stream)));
   ADAMAS_CUDA(cudaStreamSynchronize(as_stream(stream)));
   if (status) *status = h;
-  return ADAMAS_OK;
-}
-
-int adamas_cache_spec_stats(adamas_cache* c, void* stream, int64_t* listed, int64_t* fallback) {
-  if (int rc = check_cache(c)) return rc;
-  unsigned long long h[2] = {0, 0};
-  const char* src = reinterpret_cast<const char*>(c->tprev) + (size_t)c->n_kv * kMaxTprevGroup * sizeof(int);
-  ADAMAS_CUDA(cudaMemcpyAsync(h, src, sizeof(h), cudaMemcpyDeviceToHost, as_stream(stream)));
-  ADAMAS_CUDA(cudaStreamSynchronize(as_stream(stream)));
-  if (listed) *listed = (int64_t)h[0];
-  if (fallback) *fallback = (int64_t)h[1];
   return ADAMAS_OK;
 }
 

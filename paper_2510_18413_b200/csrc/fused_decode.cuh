@@ -58,17 +58,6 @@ constexpr int kPartStride = 132;  // floats per partial: m, l, pad, pad, o[128]
 constexpr int kFusedUnsupported = -100;
 constexpr int kTokPerThread = 1024 / (kConsumerWarps * 32);  // tokens per consumer thread per stage
 constexpr int kTraceTid = (kConsumerWarps - 1) * 32;  // diagnostics: the thread that takes phase stamps
-// Speculative threshold (lean instances): tokens at distance <= Tg (the
-// head's threshold T of its previous decode step plus a margin) are listed
-// during the scan, up to kCandCap per head per CTA, and only they enter the
-// histogram; the compaction then orders this short list instead of the whole
-// distance row. If the exchanged histogram does not reach k below Tg (T moved
-// up) or a list overflowed, the CTAs of the unit rebuild full histograms from
-// the distance row and take the exact full-row path: the selection is exact
-// either way, the guess only decides how much work it takes.
-constexpr int kCandCap = 512;
-constexpr int kOvfBin = kHistBins - 1;  // histogram bin carrying the list-overflow flag (distances <= 384)
-constexpr int kMaxTprevGroup = 64;      // q-heads per kv-head with a stored previous threshold
 
 struct FusedSeq {
   uint4* codes;  // this sequence's cache: [n_kv][2 planes][cap] x 16 B
@@ -78,7 +67,6 @@ struct FusedSeq {
   int64_t s_old;  // tokens in the cache before this step's append
   int64_t clean;  // tokens [0, clean) were not written by the preceding kernel: streamable before the PDL wait
   int* status;    // this cache's sticky status word
-  int* tprev;     // [n_kv * kMaxTprevGroup] previous step's threshold per q-head (-1 unknown), or null
   // multi-cluster units (FusedParams::P > 1): global scratch of this cache
   uint32_t* xhist;  // [unit][P][G][kHistBins] cluster-combined histograms
   float* xpart;     // [unit][P][G][kPartStride] cluster partials
@@ -96,7 +84,6 @@ struct FusedParams {
   PeerPush peers;    // candidates mode, peer exchange: keys go to every rank's mailbox (cand unused)
   int qsplit;        // clusters per kv-head: each scans the codes for G of its qsplit * G q-heads
   int P;             // clusters per unit (token ranges); > 1 exchanges through global memory
-  int spec_margin;   // speculative threshold Tg = previous T + margin; < 0 disables
   const void* q;      // [n_seqs][n_q][128]
   const void* k_new;  // [n_seqs][n_kv][128]
   const void* v_new;
@@ -162,14 +149,19 @@ __device__ __forceinline__ void unit_barrier(int* bar, int target, bool wait, in
 }
 
 // Named barrier over the 16 consumer warps (the producer warp never joins).
-// Non-aligned form: a warp may reach it diverged (after a divergent loop or an
-// mbarrier spin whose lanes exit on different polls); the aligned bar.sync
-// would then count the warp before all of its lanes arrived.
-__device__ __forceinline__ void consumer_sync() { asm volatile("barrier.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+// The explicit __syncwarp makes every warp converged before the aligned
+// bar.sync: a warp can reach a consumer barrier diverged (after a divergent
+// loop, or an mbarrier spin whose lanes exit on different polls), and an
+// aligned barrier reached by part of a warp released the block early
+// (measured: wrong tie counts under skewed warps).
+__device__ __forceinline__ void consumer_sync() {
+  __syncwarp();
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
 
 // Dynamic shared-memory carve-up, identical on host and device.
 struct FusedSmem {
-  uint32_t stage, dist, hist, hist_all, hist_all2, cand, sel, inbox, wpart, qf, qcode, sq, bars, total;
+  uint32_t stage, dist, hist, hist_all, sel, inbox, wpart, qf, qcode, sq, bars, total;
   __host__ __device__ static uint32_t align(uint32_t x, uint32_t a) { return (x + a - 1u) & ~(a - 1u); }
   __host__ __device__ FusedSmem(int G, int C, int chunk, int selcap, int stages, int P = 1) {
     uint32_t o = 0;
@@ -180,11 +172,6 @@ struct FusedSmem {
     // for the heads this rank owns only (two hops, C x G > 8)
     const uint32_t owned_max = (uint32_t)((G + C - 1) / C);
     hist_all = o; o += (C * G > 8 || P > 1 ? owned_max * C : (uint32_t)C * G) * kHistBins * 2;
-    // one-hop launches: a second exchange buffer (the speculative path's
-    // fallback round) and the per-head candidate lists
-    const bool one_hop = !(C * G > 8 || P > 1);
-    hist_all2 = o; o += one_hop ? (uint32_t)C * G * kHistBins * 2 : 0u;
-    cand = o;  o += one_hop ? (uint32_t)G * kCandCap * 4 : 0u;
     sel = o;   o = align(o + (uint32_t)G * selcap * 4, 16);
     inbox = o; o += owned_max * C * kPartStride * 4;  // partials of the heads this rank merges
     wpart = o; o += kConsumerWarps * kPartStride * 4;
@@ -192,7 +179,7 @@ struct FusedSmem {
     o = align(o, 32);
     qcode = o; o += (uint32_t)(G + 1) * 32;
     sq = o;    o += (uint32_t)(G + 1) * kHeadDim * 8;
-    bars = o;  o += (2 * kMaxStages + 4) * 8;  // full[], empty[], hist / partial / threshold / fallback exchange
+    bars = o;  o += (2 * kMaxStages + 3) * 8;  // full[], empty[], hist / partial / threshold exchange
     total = o;
   }
 };
@@ -303,7 +290,6 @@ __device__ __forceinline__ bool encode128_to(const float in[4], double* sq, Code
 template <typename T, int G, int SW, bool FULL, int CT>
 __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel(const __grid_constant__ FusedParams p) {
   static_assert(G >= 1 && G <= kMaxG && (kConsumerWarps % G) == 0, "G must divide the warp count");
-  constexpr bool SPEC = !FULL && SW > 0;  // speculative-threshold candidate lists (see kCandCap)
   constexpr int WG = kConsumerWarps / G;  // consumer warps per q-head
   constexpr int NT = kConsumers / G;      // consumer threads per q-head
   extern __shared__ __align__(128) uint8_t smem[];
@@ -313,7 +299,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   __shared__ int rank_cnt[16][2];              // two-hop exchange, owner side: per rank (< T, == T)
   __shared__ int cl_cnt[2];                    // multi-cluster unit: earlier clusters' (< T, == T)
   __shared__ int nsel[kMaxG];
-  __shared__ int cand_n[kMaxG], tg_s[kMaxG];  // speculative path: list lengths, guessed thresholds Tg
   const int C = CT > 0 ? CT : p.C;
   const int rank = (int)cluster_rank();
   const int P = FULL ? p.P : 1;
@@ -357,9 +342,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   uint64_t* hist_bar = full_bar + 2 * kMaxStages;
   uint64_t* inbox_bar = hist_bar + 1;
   uint64_t* sc_bar = hist_bar + 2;
-  uint64_t* hist_bar2 = hist_bar + 3;  // the speculative path's fallback exchange
-  uint16_t* hist_all2 = reinterpret_cast<uint16_t*>(smem + L.hist_all2);
-  uint32_t* cand = reinterpret_cast<uint32_t*>(smem + L.cand);  // [G][kCandCap] (distance << 16 | local token)
   const bool two_hop = FULL && (C * G > 8 || P > 1);  // histogram exchange topology (see the select phase)
   const int xunit = hk * p.qsplit + part;     // this cache's unit index (global scratch)
   const int owners = min(C, G);               // ranks of a cluster that own a head
@@ -399,15 +381,12 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     mbar_init(hist_bar, 1);
     mbar_init(inbox_bar, 1);
     mbar_init(sc_bar, 1);
-    mbar_init(hist_bar2, 1);
     mbar_fence_init();
     for (int st = 0; st < min(ring, n_stages); ++st) issue(st, st);
     // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
     // C partials per q-head it merges
     if (!two_hop) mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
     else if (n_owned) mbar_expect_tx(hist_bar, (uint32_t)(n_owned * C * kHistBins * 2));
-    // armed always, completed only if the unit falls back (then every rank pushes)
-    if (SPEC) mbar_expect_tx(hist_bar2, (uint32_t)(C * G * kHistBins * 2));
     if (two_hop) mbar_expect_tx(sc_bar, (uint32_t)(G * 16));
     if (n_owned && !pcand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
   }
@@ -453,19 +432,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 
   if (warp < G) {  // encode query head hk * G + warp (sweep.cpp:92-94)
     *reinterpret_cast<float4*>(qfs + warp * kHeadDim + lane * 4) = make_float4(f[0], f[1], f[2], f[3]);
-    if (lane == 0) {
-      if (SPEC) {  // Tg = this q-head's previous T + margin (written by an earlier, completed launch)
-        sc[warp][0] = -1;  // T not found yet
-        const int* tp = p.seq[si].tprev;
-        int t = -1;
-        if (tp != nullptr && p.spec_margin >= 0) {
-          const int v = tp[hk * kMaxTprevGroup + part * G + warp];
-          if (v >= 0) t = min(v + p.spec_margin, 3 * kHeadDim);
-        }
-        tg_s[warp] = t;
-        cand_n[warp] = 0;
-      }
-    }
     Code c;
     ADAMAS_TRACE(12);
     if (pdbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
@@ -510,25 +476,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   int jslot[kTokPerThread];
 #pragma unroll
   for (int u = 0; u < kTokPerThread; ++u) jslot[u] = dslot(tid + u * kConsumers);
-  int tgr[G];  // speculative thresholds (-1: no candidates, everything falls back)
-#pragma unroll
-  for (int g = 0; g < G; ++g) tgr[g] = SPEC ? tg_s[g] : 0;
-  const T* const Kspan = reinterpret_cast<const T*>(p.seq[si].K) + ((int64_t)hk * cap + start) * kHeadDim;
-  const T* const Vspan = reinterpret_cast<const T*>(p.seq[si].V) + ((int64_t)hk * cap + start) * kHeadDim;
-  // a listed candidate: counted, listed (token order restored by the
-  // compaction) and its K / V rows warmed in L2 for the gather
-  auto take_candidate = [&](int g, uint32_t dd, int x) {
-    atomicAdd(&hist[g * kHistBins + dd], 1);
-    const int slot_c = atomicAdd(&cand_n[g], 1);
-    if (slot_c < kCandCap) cand[g * kCandCap + slot_c] = (dd << 16) | (uint32_t)x;
-    const char* kp = reinterpret_cast<const char*>(Kspan + (int64_t)x * kHeadDim);
-    const char* vp = reinterpret_cast<const char*>(Vspan + (int64_t)x * kHeadDim);
-#pragma unroll
-    for (int c = 0; c < (int)(kHeadDim * sizeof(T)); c += 128) {
-      prefetch_l2(kp + c);
-      prefetch_l2(vp + c);
-    }
-  };
 
   // ---------------------------------------------------------------- scan
   ADAMAS_TRACE(2);
@@ -562,8 +509,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           dist[g * p.chunk + base + jslot[u]] = (uint16_t)d[u][g];
-          if (!SPEC) atomicAdd(&hist[g * kHistBins + d[u][g]], 1);
-          else if ((int)d[u][g] <= tgr[g]) take_candidate(g, d[u][g], base + j);
+          atomicAdd(&hist[g * kHistBins + d[u][g]], 1);
         }
       }
     }
@@ -579,49 +525,42 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     for (int w = 0; w < 4; ++w) nx[w] = nc.lo[w] ^ nc.hi[w];
     const uint32_t d = l1_distance(make_qcode(qcode[tid]), nc.lo, nx);
     dist[tid * p.chunk + dslot((int)(s_old - start))] = (uint16_t)d;
-    if (!SPEC) atomicAdd(&hist[tid * kHistBins + d], 1);
-    else if ((int)d <= tgr[tid]) take_candidate(tid, d, (int)(s_old - start));
+    atomicAdd(&hist[tid * kHistBins + d], 1);
   }
   consumer_sync();  // local histogram final
-#if ADAMAS_DIAG
-  if ((pdbg & (1 << 20)) && ptrace != nullptr && blockIdx.x == 0)  // diagnostics: the distance row after the scan
-    for (int x = tid; x < G * p.chunk; x += kConsumers) reinterpret_cast<uint16_t*>(ptrace)[x] = dist[x];
-#endif
-
   ADAMAS_TRACE(3);
   const int k_eff = (int)min((int64_t)p.budget, S);
   const int g_me = tid / NT, t_in = tid % NT;
   cluster_wait();
-  // One hop: every rank's histograms (u16: counts <= chunk < 2^16) go to
-  // every rank (st.async; each receiver's mbarrier counts bytes); each rank
-  // then derives, per head, T, the count below T and its own offsets.
-  auto push_hists = [&](uint16_t* dst_buf, uint64_t* bar) {
+  if (!two_hop) {
+    // One hop: every rank's histograms (u16: counts <= chunk < 2^16) go to
+    // every rank (st.async; each receiver's mbarrier counts bytes); each rank
+    // then derives, per head, T, the count below T and its own offsets.
     if (tid < G * (kHistBins / 8)) {
       const int g = tid / (kHistBins / 8), b0 = (tid % (kHistBins / 8)) * 8;
       const int4 h0 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0);
       const int4 h1 = *reinterpret_cast<const int4*>(hist + g * kHistBins + b0 + 4);
-      // the overflow bin (no distance reaches it) carries "this rank's list overflowed"
-      const int last = (SPEC && b0 + 7 == kOvfBin) ? (cand_n[g] > kCandCap ? 1 : 0) : h1.w;
       const uint32_t w0 = (uint32_t)h0.x | ((uint32_t)h0.y << 16), w1 = (uint32_t)h0.z | ((uint32_t)h0.w << 16);
-      const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)last << 16);
-      const uint32_t local = smem_addr(dst_buf + ((size_t)rank * G + g) * kHistBins + b0);
+      const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)h1.w << 16);
+      const uint32_t local = smem_addr(hist_all + ((size_t)rank * G + g) * kHistBins + b0);
       for (int r = 0; r < C; ++r)
-        st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(bar), r));
+        st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), r));
     }
-  };
-  // Head g's T = smallest distance whose cumulative count over all ranks
-  // reaches k. NT threads per head, G consecutive bins each; a head-segmented
-  // block prefix orders the threads; the owning thread walks its bins.
-  auto search_hists = [&](const uint16_t* src_buf) {
+    mbar_wait(hist_bar, 0);
+    ADAMAS_TRACE(4);
+
+    // Head g's T = smallest distance whose cumulative count over all ranks
+    // reaches k. NT threads per head, G consecutive bins each; a head-segmented
+    // block prefix orders the threads; the owning thread walks its bins.
     const int b0 = t_in * G;
     int tot[G], pre[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) { tot[i] = 0; pre[i] = 0; }
     for (int r = 0; r < C; ++r) {
-      const uint16_t* h = src_buf + ((size_t)r * G + g_me) * kHistBins + b0;
+      const uint16_t* h = hist_all + ((size_t)r * G + g_me) * kHistBins + b0;
 #pragma unroll
       for (int i = 0; i < G; ++i) {
-        const int v = (SPEC && b0 + i == kOvfBin) ? 0 : h[i];
+        const int v = h[i];
         tot[i] += v;
         pre[i] += r < rank ? v : 0;
       }
@@ -642,33 +581,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         }
         c += tot[i];
         cp += pre[i];
-      }
-    }
-  };
-  bool fallback = false;  // speculative path missed: full-row histograms and compaction
-  if (!two_hop) {
-    push_hists(hist_all, hist_bar);
-    mbar_wait(hist_bar, 0);
-    ADAMAS_TRACE(4);
-    search_hists(hist_all);
-    if (SPEC) {
-      consumer_sync();  // sc final
-      // T above every rank's guess (k not reached below Tg), or a rank's list
-      // overflowed: the same decision on every rank (same exchanged data)
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        fallback |= sc[g][0] < 0;
-        for (int r = 0; r < C; ++r) fallback |= hist_all[((size_t)r * G + g) * kHistBins + kOvfBin] != 0;
-      }
-      if (fallback) {  // rebuild this rank's full histograms from the distance row, exchange again
-        for (int i = tid; i < G * kHistBins; i += kConsumers) hist[i] = 0;
-        consumer_sync();
-        for (int g = 0; g < G; ++g)
-          for (int x = tid; x < len; x += kConsumers) atomicAdd(&hist[g * kHistBins + dist[g * p.chunk + dslot(x)]], 1);
-        consumer_sync();
-        push_hists(hist_all2, hist_bar2);
-        mbar_wait(hist_bar2, 0);
-        search_hists(hist_all2);
       }
     }
   } else {
@@ -757,62 +669,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   // swizzled distance layout, see before the scan) keep their masks in
   // registers between the two passes; longer ranks take 32-token groups per
   // thread and recompute the masks.
-  if (SPEC && !fallback) {
-    // Speculative path: every selected token is in the head's candidate list
-    // (distance <= T <= Tg). The listed tokens at distance <= T are marked in
-    // a per-head bitmap over the rank (in the ring, idle after the scan);
-    // thread t_in of the head owns a contiguous run of bitmap words, so a
-    // head-segmented prefix of its (< T, == T) counts gives every marked
-    // token its output position in index order, with the ties at T taken up
-    // to the tie budget: top_k's (score, index) order (estimator.cpp:75-90).
-    const int g = g_me;
-    const int thr = sc[g][0], below = sc[g][1], pre_lt = sc[g][2], pre_eq = sc[g][3];
-    const int need = k_eff - below;
-    const int eq_budget = max(0, need - pre_eq);
-    const int out_off = pre_lt + min(pre_eq, need);
-    const int words = (len + 31) >> 5;
-    uint32_t* bm = reinterpret_cast<uint32_t*>(smem + L.stage);  // [G][words]
-    for (int i = tid; i < G * words; i += kConsumers) bm[i] = 0u;
-    consumer_sync();
-    const int n = min(cand_n[g], kCandCap);
-    for (int i = t_in; i < n; i += NT) {
-      const uint32_t e = cand[g * kCandCap + i];
-      const int tok = (int)(e & 0xffffu);
-      if ((int)(e >> 16) <= thr) atomicOr(&bm[g * words + (tok >> 5)], 1u << (tok & 31));
-    }
-    consumer_sync();
-    const uint16_t* dg = dist + g * p.chunk;
-    const int wpt = (words + NT - 1) / NT;
-    const int w0 = min(words, t_in * wpt), w1 = min(words, w0 + wpt);
-    int my_lt = 0, my_eq = 0;
-    for (int w = w0; w < w1; ++w)
-      for (uint32_t m = bm[g * words + w]; m; m &= m - 1) {
-        const int x = w * 32 + __ffs(m) - 1;
-        if ((int)dg[dslot(x)] < thr) ++my_lt;
-        else ++my_eq;
-      }
-    int lt_before, eq_before, lt_tot, eq_tot;
-    head_scan2<G>(my_lt, my_eq, lt_before, eq_before, lt_tot, eq_tot, scratch);
-    if (t_in == 0) nsel[g] = min(lt_tot + min(eq_tot, eq_budget), selcap);
-    if (my_lt > 0 || (my_eq > 0 && eq_before < eq_budget)) {
-      int32_t* idx_row = (p.idx && !(pdbg & 2)) ? p.idx + ((int64_t)si * n_q + q0 + g) * p.budget + out_off : nullptr;
-      int pos = lt_before + min(eq_before, eq_budget);
-      int eq_seen = eq_before;
-      for (int w = w0; w < w1; ++w)
-        for (uint32_t m = bm[g * words + w]; m; m &= m - 1) {
-          const int x = w * 32 + __ffs(m) - 1;
-          if ((int)dg[dslot(x)] == thr && eq_seen++ >= eq_budget) continue;  // ties beyond the budget
-          const int t = (int)start + x;
-          if (pos < selcap) sel[g * selcap + pos] = t;
-          if (idx_row) idx_row[pos] = t;
-          ++pos;
-        }
-    }
-    if (gr == 0 && p.idx && t_in == 0) {  // estimator.cpp:80 caps the selection at S
-      int32_t* row = p.idx + ((int64_t)si * n_q + q0 + g) * p.budget;
-      for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
-    }
-  } else {
+  {
     const int g = g_me;
     const int ngroups = (len + 31) >> 5;
     const int gpt = (ngroups + NT - 1) / NT;
@@ -942,14 +799,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       } else {
         for (int i = k_eff; i < p.budget; ++i) pcand[row + i] = 0xffffffffu;
       }
-    }
-  }
-  if (p.seq[si].tprev != nullptr && gr == 0 && tid < G) {  // the next step's guess
-    p.seq[si].tprev[hk * kMaxTprevGroup + part * G + tid] = sc[tid][0];
-    if (SPEC && tid == 0) {  // per-cache counters after the guesses: [listed path, fallback] per unit step
-      unsigned long long* stats =
-          reinterpret_cast<unsigned long long*>(p.seq[si].tprev + (size_t)p.n_kv * kMaxTprevGroup);
-      atomicAdd(stats + (fallback ? 1 : 0), 1ull);
     }
   }
   consumer_sync();
@@ -1116,17 +965,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       }
     }
   }
-#if ADAMAS_DIAG
-  if ((pdbg & (1 << 20)) && ptrace != nullptr && blockIdx.x == 0) {  // diagnostics: the row at the end, and T
-    consumer_sync();
-    for (int x = tid; x < G * p.chunk; x += kConsumers) reinterpret_cast<uint16_t*>(ptrace)[262144 + x] = dist[x];
-    if (tid < G) reinterpret_cast<int*>(ptrace)[200000 + tid] = sc[tid][0];
-    if (tid < G) reinterpret_cast<int*>(ptrace)[200008 + tid] = fallback ? 1 : 0;
-    if (tid < G) reinterpret_cast<int*>(ptrace)[200016 + tid] = nsel[tid];
-    if (tid < G) reinterpret_cast<int*>(ptrace)[200024 + tid] = sc[tid][1];
-    for (int i = tid; i < G * selcap; i += kConsumers) reinterpret_cast<int*>(ptrace)[210000 + i] = sel[i];
-  }
-#endif
   ADAMAS_TRACE(11);
   if (ptrace != nullptr && tid == kTraceTid && !(pdbg & 32)) ptrace[blockIdx.x * 16 + 15] = trace_clock(pdbg);
 }

@@ -1,15 +1,18 @@
-"""-m gpu: the speculative-threshold path of the fused decode step.
+"""-m gpu: many consecutive fused decode steps on one cache with queries whose
+threshold jumps from step to step (random queries, queries close to a cached
+key, back to random), heavy ties, budgets above the length, and the rank
+lengths that need ring refills (more stages than the ring holds). Every step's
+selection must equal the reference's top_k (estimator.cpp:75-90) exactly.
 
-From its second step on, a cache lists only the tokens at distance <= Tg (the
-q-head's previous threshold T plus a margin) during the scan; if T moved above
-Tg or a list overflowed, the unit falls back to the full-row selection. Either
-way the selection must equal the reference's top_k (estimator.cpp:75-90)
-exactly. These tests drive hits, misses (T jumping up), T jumping down, list
-overflow (dense ties) and the margin settings over many consecutive steps."""
+These cases exposed a barrier bug during development: an aligned bar.sync
+reached by a diverged warp released the consumer warps early and the tie
+count below T came out wrong under skewed warps (fixed by converging each warp
+before the named barrier, fused_decode.cuh consumer_sync)."""
 import numpy as np
 import pytest
 import torch
 
+from oracle.bindings import bf16_round
 from tests.gpu_helpers import make_inputs, oracle_decode, rel_err, to_dev
 
 pytestmark = pytest.mark.gpu
@@ -37,7 +40,7 @@ def _steps(gpu, oracle, K, V, qs, budget, bf16):
 
 def _mixed_queries(K, n_q, n_kv, steps, bf16, seed):
     """random queries, interleaved with queries close to a cached key (their
-    T drops far below the previous step's) and back (T jumps above Tg)"""
+    T drops far below the previous step's) and back (T jumps up)"""
     rng = np.random.default_rng(seed)
     G = n_q // n_kv
     qs = []
@@ -48,31 +51,28 @@ def _mixed_queries(K, n_q, n_kv, steps, bf16, seed):
                 src = K[rng.integers(0, K.shape[0] - steps), h // G]
                 q[h] = src + 0.05 * q[h]
         if bf16:
-            from oracle.bindings import bf16_round
             q = bf16_round(q)
         qs.append(q.astype(np.float32))
     return qs
 
 
-@pytest.mark.parametrize("margin", [-1, 0, 2, 6, 40])
-@pytest.mark.parametrize("S,n_kv,G,budget,cluster", [(20000, 2, 1, 128, 4), (12000, 2, 4, 64, 2), (9000, 1, 2, 200, 1)])
-def test_spec_mixed_steps(gpu, oracle, tune, margin, S, n_kv, G, budget, cluster):
-    tune(spec_margin=margin, cluster=cluster)
-    steps = 9
-    K, V, _ = make_inputs(S + steps, n_kv, n_kv * G, True, S + margin + 3)
+@pytest.mark.parametrize("S,n_kv,G,budget,cluster,stages", [
+    (20000, 2, 1, 128, 4, 0), (12000, 2, 4, 64, 2, 0), (9000, 1, 2, 200, 1, 0),
+    (8000, 2, 1, 64, 1, 2),    # 8 stages through a 2-slot ring
+    (24000, 2, 1, 64, 4, 2),
+    (12000, 2, 2, 64, 1, 3),
+])
+def test_multistep_mixed_queries(gpu, oracle, tune, S, n_kv, G, budget, cluster, stages):
+    tune(cluster=cluster, stages=stages)
+    steps = 7
+    K, V, _ = make_inputs(S + steps, n_kv, n_kv * G, True, S + 3)
     qs = _mixed_queries(K, n_kv * G, n_kv, steps, True, S + G)
-    cache = _steps(gpu, oracle, K, V, qs, budget, True)
-    listed, fallback = cache.spec_stats()
-    if margin < 0:
-        assert listed == 0
-    elif margin in (2, 6):
-        assert listed > 0, (listed, fallback)  # random steps after random steps hit
+    _steps(gpu, oracle, K, V, qs, budget, True)
 
 
 @pytest.mark.parametrize("cluster", [1, 4])
-def test_spec_list_overflow_dense_ties(gpu, oracle, tune, cluster):
-    """keys from 4 distinct vectors: thousands of tokens share each distance,
-    so the candidate lists overflow on every step after the first"""
+def test_multistep_dense_ties(gpu, oracle, tune, cluster):
+    """keys from 4 distinct vectors: thousands of tokens share each distance"""
     tune(cluster=cluster)
     S, n_kv, G, budget, steps = 8000, 1, 2, 100, 4
     K, V, _ = make_inputs(S + steps, n_kv, n_kv * G, False, 77)
@@ -82,22 +82,9 @@ def test_spec_list_overflow_dense_ties(gpu, oracle, tune, cluster):
     _steps(gpu, oracle, K, V, qs, budget, False)
 
 
-def test_spec_budget_above_length(gpu, oracle, tune):
-    """budget > S: T is the largest distance, far above any guess"""
+def test_multistep_budget_above_length(gpu, oracle, tune):
     tune(cluster=1)
     S, n_kv, G, budget, steps = 300, 1, 1, 512, 4
     K, V, _ = make_inputs(S + steps, n_kv, n_kv * G, True, 5)
     qs = [make_inputs(1, 1, n_kv * G, True, 900 + st)[2] for st in range(steps)]
     _steps(gpu, oracle, K, V, qs, budget, True)
-
-
-def test_spec_repeated_query_hits(gpu, oracle, tune):
-    """the same query every step: T stays put and every step after the first
-    takes the listed path (margin 0: Tg == T)"""
-    tune(spec_margin=0, cluster=4)
-    S, n_kv, G, budget, steps = 16000, 2, 1, 128, 5
-    K, V, _ = make_inputs(S + steps, n_kv, n_kv * G, True, 31)
-    q = make_inputs(1, 1, n_kv * G, True, 32)[2]
-    cache = _steps(gpu, oracle, K, V, [q] * steps, budget, True)
-    listed, fallback = cache.spec_stats()
-    assert fallback == n_kv and listed == n_kv * (steps - 1), (listed, fallback)  # only the first step falls back
