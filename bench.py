@@ -86,15 +86,20 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def load_traffic():
-    """dram bytes per launch of the fused kernel from the committed ncu summary."""
+TRAFFIC_KEY = {"longchat": "fused_decode_kernel", "llama128k": "fused_decode_kernel[llama128k]",
+               "batched16": "fused_decode_kernel[batched16]",
+               "seqshard1m": "fused_decode_kernel[seqshard1m candidates]"}
+
+
+def load_traffic(config="longchat"):
+    """dram bytes per launch of the config's fused kernel from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("fused_decode_kernel", {}).get("dram_bytes_per_launch")
+        return d.get(TRAFFIC_KEY.get(config, ""), {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -371,22 +376,35 @@ def run_ours(args):
             gather = torch_allgather() if ws > 1 else None
             keys_all = torch.empty((L, n_virtual, n_q, B), dtype=torch.int32, device="cuda")
             parts_all = torch.empty((L, n_virtual, n_q, 132), dtype=torch.float32, device="cuda")
-            shard_off = ((torch.arange(n_virtual, device="cuda", dtype=torch.int32) - my_slot) * S).view(-1, 1, 1)
+            if gather is None:
+                # N = 1: the other 7 shards' slots of the gathered keys and partials are filled ONCE, before
+                # the timed region, from this shard's first step (same distances, indices moved to their
+                # ranges); each timed step's kernels write this rank's slot in place, so the step is exactly
+                # this rank's three launches (candidates, select/attend, merge) with no data-path copies
+                shard_off = ((torch.arange(n_virtual, device="cuda", dtype=torch.int32) - my_slot) * S).view(-1, 1, 1)
+                for l in range(L):
+                    c = caches[l][0]
+                    k0 = ops.local_candidates(c, qs[0, l, 0], ks[0, l, 0], vs[0, l, 0], tail, base, B)
+                    keys_all[l].copy_(k0.unsqueeze(0) + shard_off)
+                    p0, _ = ops.select_attend(c, qs[0, l, 0], keys_all[l], B, n_virtual * S, base)
+                    parts_all[l].copy_(p0.unsqueeze(0).expand(n_virtual, -1, -1))
+                    if tail:
+                        c.truncate(S - 1)
 
             def step(s, st):
                 for l in range(L):
                     c = caches[l][0]
-                    keys = ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], tail, base, B, stream=st)
                     if gather is not None:
+                        keys = ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], tail, base, B, stream=st)
                         keys_all[l].copy_(gather(keys))
-                    else:  # other shards: same distances, indices moved to their ranges (one kernel)
-                        torch.add(keys.unsqueeze(0), shard_off, out=keys_all[l])
-                    part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
-                    if gather is not None:
+                        part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
                         parts_all[l].copy_(gather(part))
                     else:
-                        parts_all[l].copy_(part.unsqueeze(0).expand(n_virtual, -1, -1))
-                    out[l, 0].copy_(ops.lse_merge(parts_all[l], stream=st))
+                        ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], tail, base, B, stream=st,
+                                             out=keys_all[l, my_slot])
+                        ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st,
+                                          out=parts_all[l, my_slot])
+                    ops.lse_merge(parts_all[l], stream=st, out=out[l, 0])
                     if tail:
                         c.truncate(S - 1)
     else:
@@ -508,7 +526,7 @@ def run_ours(args):
         bytes_launch = n_kv * S * 32 + n_q * (B // 8) * 2 * 128 * es
     achieved = bytes_launch / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = load_peaks()
-    traffic = load_traffic() if args.config == "longchat" else None
+    traffic = load_traffic(args.config)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config == "longchat":
@@ -536,7 +554,8 @@ def run_ours(args):
                              f"{L * NS * n_kv * S * (256 * es + 32) / 2**30:.1f} GiB > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "frac_of_8tbs": achieved / 8000.0,
-                         "kernel": "fused_decode_kernel", "bytes_per_launch": bytes_launch,
+                         "kernel": ("fused candidates + seq_select_attend + lse_merge (3 launches per layer)"
+                                    if seqshard else "fused_decode_kernel"), "bytes_per_launch": bytes_launch,
                          "kernel_us": kern_ms * 1000.0, "peak_source": peak_kind},
             "e2e": {"value": e2e_ms * 1000.0 / (n_e2e * L * tokens_per_layer), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

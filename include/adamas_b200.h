@@ -198,7 +198,12 @@ int adamas_seq_local_candidates(adamas_cache* cache, const void* q, int n_q_head
  * rank's survivors, float32 [n_q][132] = (m in natural-log units, l, 0, 0,
  * o[128] unnormalised), and optionally the global selection int32
  * [n_q][budget] ascending (-1 past min(budget, total_len)).
- * n_ranks * budget <= 8192, budget <= 2048. */
+ * n_ranks * budget <= 8192, budget <= 2048. Input contract (what
+ * adamas_seq_local_candidates produces): each rank's keys ascending in the
+ * index field with empty keys (0xffffffff) last, ranks in sequence order; the
+ * selection is then an order-preserving compaction (no sort). Keys violating
+ * it latch ADAMAS_STATUS_BAD_SELECTION in the cache status and the launch
+ * writes nothing. */
 int adamas_seq_select_attend(const adamas_cache* cache, const void* q, int n_q_heads, const uint32_t* gathered,
                              int n_ranks, int64_t budget, int64_t total_len, int64_t rank_base, float* partial,
                              int32_t* global_idx, void* stream);

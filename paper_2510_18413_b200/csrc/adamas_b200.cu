@@ -106,8 +106,9 @@ template <typename T>
 int launch_append(adamas_cache* c, const void* keys, const void* values, const uint16_t* codes_ref,
                   int64_t n_tokens, cudaStream_t s) {
   const int64_t n_vec = n_tokens * c->n_kv;
-  const int64_t blocks_needed = (n_vec + 2 * kAppendWarps - 1) / (2 * kAppendWarps);  // 2 vectors per warp
-  const int grid = (int)std::min<int64_t>(blocks_needed, (int64_t)sm_count() * 16);
+  const int64_t warp_blocks = (n_tokens + kAppendNV - 1) / kAppendNV * c->n_kv;  // (token block, kv-head) per warp
+  const int64_t blocks_needed = (warp_blocks + kAppendWarps - 1) / kAppendWarps;
+  const int grid = (int)std::min<int64_t>(blocks_needed, (int64_t)sm_count() * 4);  // a resident grid, loops
   if (codes_ref)
     append_kernel<T, true><<<grid, kAppendWarps * 32, 0, s>>>(
         (const T*)keys, (const T*)values, codes_ref, n_vec, c->n_kv, c->seq_len, c->capacity, (T*)c->K,
@@ -300,18 +301,82 @@ struct FusedPlan {
   size_t smem = 0;
 };
 
+// Clusters of C CTAs with `smem` bytes of dynamic shared memory each that
+// co-reside on this device (cudaOccupancyMaxActiveClusters of a fused-kernel
+// instance: one 544-thread CTA per SM, so the shared-memory size decides).
+// Measured on B200 at ~200 KB: 33 clusters of 4, 15 of 8, 7 of 16 (not 148 / C:
+// clusters must fit inside a GPC).
+int max_active_clusters(int C, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, std::pair<int, size_t>>, int>> memo;  // ((dev, (C, smem)) -> n)
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : memo)
+    if (e.first.first == dev && e.first.second.first == C && e.first.second.second == smem) return e.second;
+  auto kern = fused_decode_kernel<__nv_bfloat16, 1, 0, true, 0>;
+  {  // configure it for the largest size once (launches of this instance never lower it)
+    std::lock_guard<std::mutex> flock(g_facts_mu);
+    KernelFacts& kf = kernel_facts((const void*)kern, dev);
+    const size_t max_smem = 220 * 1024;
+    if (kf.smem_configured < max_smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      kf.smem_configured = max_smem;
+    }
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)C);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = sm_count() / C;  // unknown: assume a full machine
+  }
+  memo.push_back({{dev, {C, smem}}, n});
+  return n;
+}
+
 // C CTAs per (sequence, kv-head, q-split part) unit and the per-rank chunk
 // for a fixed q-split. P > 1 (opt-in) exchanges histograms and partials
 // through global memory with a self-resetting barrier; it is exact but
 // measured slower than splitting the q-heads (qsplit), so the automatic
 // choice grows C only.
+FusedPlan plan_for_split_c(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, int C,
+                           const Tuning& tu);
+
+// The automatic cluster size: the largest C (up to 16) whose grid still fits
+// the machine, grown when the rank's chunk does not fit shared memory, then
+// shrunk while the clusters would not all co-reside (a grid of more clusters
+// than fit runs in two waves: measured 16 x 8-CTA clusters 16.1 us vs 16 x 4
+// at 9.2 us per layer for 16 heads of 32K).
 FusedPlan plan_for_split(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, const Tuning& tu) {
+  FusedPlan pl = plan_for_split_c(n_seqs, n_kv, n_q, s_max, budget, qsplit, tu.cluster, tu);
+  if (!pl.ok || tu.cluster > 0) return pl;
+  const int64_t clusters = (int64_t)n_seqs * n_kv * qsplit * pl.P;
+  if (clusters * pl.C > sm_count() || clusters <= max_active_clusters(pl.C, pl.smem)) return pl;
+  for (int C = pl.C / 2; C >= 1; C /= 2) {
+    const FusedPlan q = plan_for_split_c(n_seqs, n_kv, n_q, s_max, budget, qsplit, C, tu);
+    if (q.ok && q.C == C && clusters <= max_active_clusters(C, q.smem)) return q;
+  }
+  return pl;
+}
+
+FusedPlan plan_for_split_c(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, int C_req,
+                           const Tuning& tu) {
   FusedPlan pl;
   const int G = n_q / (n_kv * qsplit);
   if (n_q % (n_kv * qsplit) || (G != 1 && G != 2 && G != 4 && G != 8)) return pl;
   if (n_seqs > kMaxSeqs || budget > (1 << 20)) return pl;
   const int units = n_seqs * n_kv * qsplit;
-  int C = tu.cluster;
+  int C = C_req;
   if (C <= 0) {
     C = 1;
     while (C < 16 && units * C * 2 <= sm_count()) C *= 2;
@@ -351,28 +416,29 @@ FusedPlan plan_for_split(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t b
   }
 }
 
-// The automatic q-split: clusters above 4 CTAs do not reach a full wave of
-// co-resident CTAs on B200 (measured), so take the smallest split of a
-// kv-head's q-heads over clusters (each re-reads the codes) whose launch uses
-// C <= 4; with more than one wave of CTAs, splitting the q-heads beats
-// splitting the tokens at the same CTA count (measured: 16 x 32K Llama batch,
-// qsplit 1 x C 2 101 us vs qsplit 2 x C 1 87 us per layer-step).
+// The automatic q-split (each q-split part re-reads the kv-head's codes for
+// its share of the q-heads): among the plans whose clusters all co-reside in
+// one wave, the one with the most CTAs (the most SMs streaming), then the
+// smallest split; if no plan fits one wave, the one with the smallest cluster
+// (measured: 16 x 32K Llama batch, qsplit 1 x C 2 101 us vs qsplit 2 x C 1 87 us
+// per layer-step), then the smallest split.
 FusedPlan plan_fused(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t budget, int qsplit, const Tuning& tu) {
   if (qsplit > 0) return plan_for_split(n_seqs, n_kv, n_q, s_max, budget, qsplit, tu);
   if (tu.qsplit > 0) return plan_for_split(n_seqs, n_kv, n_q, s_max, budget, tu.qsplit, tu);
   const int G_all = n_q / n_kv;
   FusedPlan best;
+  int64_t best_key[3] = {0, 0, 0};
   for (int qs = 1; qs <= G_all; qs *= 2) {
     if (G_all % qs) break;
     const FusedPlan pl = plan_for_split(n_seqs, n_kv, n_q, s_max, budget, qs, tu);
     if (!pl.ok) continue;
-    if (pl.C <= 4) { best = pl; break; }
-    if (!best.ok || pl.C < best.C) best = pl;
-  }
-  if (best.ok && best.C > 1 && (int64_t)n_seqs * n_kv * best.qsplit * best.C > sm_count() &&
-      G_all % (2 * best.qsplit) == 0) {
-    const FusedPlan p2 = plan_for_split(n_seqs, n_kv, n_q, s_max, budget, 2 * best.qsplit, tu);
-    if (p2.ok && p2.C < best.C) best = p2;
+    const int64_t clusters = (int64_t)n_seqs * n_kv * qs * pl.P;
+    const bool one_wave = clusters * pl.C <= sm_count() && clusters <= max_active_clusters(pl.C, pl.smem);
+    const int64_t key[3] = {one_wave ? 0 : 1, one_wave ? -clusters * pl.C : pl.C, qs};
+    if (!best.ok || std::lexicographical_compare(key, key + 3, best_key, best_key + 3)) {
+      best = pl;
+      std::copy(key, key + 3, best_key);
+    }
   }
   return best;
 }

@@ -37,6 +37,9 @@ namespace adamas_dev {
 #ifndef ADAMAS_DIAG
 #define ADAMAS_DIAG 0  // 1: phase stamps and timing-only switches (ADAMAS_DBG) compiled in (build.py --diag)
 #endif
+#ifndef ADAMAS_L2PF
+#define ADAMAS_L2PF 0  // experiments: 1 = L2 bulk prefetch of the rank's clean codes beyond the ring at CTA start
+#endif
 #ifndef ADAMAS_GATHER_PREFETCH
 #define ADAMAS_GATHER_PREFETCH 2  // L2-prefetch the gather rows: 1 all rows <= T in the count pass, 2 survivors in the emit, 0 none
 #endif
@@ -383,12 +386,22 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     mbar_init(sc_bar, 1);
     mbar_fence_init();
     for (int st = 0; st < min(ring, n_stages); ++st) issue(st, st);
+    if (ADAMAS_L2PF) {  // the rest of the clean range toward L2 while the launch waits for its predecessor
+      for (int st = ring; st < n_stages; ++st) {
+        const int ntok = min(kStageTok, clean_local - st * kStageTok);
+        if (ntok <= 0) break;
+        bulk_prefetch_l2(lo_g + (int64_t)st * kStageTok, (uint32_t)ntok * 16u);
+        bulk_prefetch_l2(x_g + (int64_t)st * kStageTok, (uint32_t)ntok * 16u);
+      }
+    }
     // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
     // C partials per q-head it merges
-    if (!two_hop) mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
-    else if (n_owned) mbar_expect_tx(hist_bar, (uint32_t)(n_owned * C * kHistBins * 2));
+    // (a single-CTA unit exchanges through its own shared memory: plain stores
+    // and the consumer barrier, no st.async, which needs a cluster of >= 2)
+    if (C > 1 && !two_hop) mbar_expect_tx(hist_bar, (uint32_t)(C * G * kHistBins * 2));
+    else if (C > 1 && n_owned) mbar_expect_tx(hist_bar, (uint32_t)(n_owned * C * kHistBins * 2));
     if (two_hop) mbar_expect_tx(sc_bar, (uint32_t)(G * 16));
-    if (n_owned && !pcand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
+    if (C > 1 && n_owned && !pcand) mbar_expect_tx(inbox_bar, (uint32_t)(n_owned * C * kPartStride * 4));
   }
   // the G query heads (and the new key) are loaded before the barrier so the
   // global-load latency overlaps the barrier initialisation
@@ -420,6 +433,10 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       uint32_t phase = 0u;  // of the slot's previous use: ((st / ring) - 1) & 1
       for (int st = ring; st < n_stages; ++st) {
         mbar_wait_backoff(&empty_bar[slot], phase);
+        // the consumers' generic-proxy reads of the slot (released through
+        // the empty barrier) are ordered before the bulk copy's async-proxy
+        // writes that refill it
+        fence_proxy_async_shared();
         issue(st, slot);
         if (++slot == ring) {
           slot = 0;
@@ -544,9 +561,11 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       const uint32_t w2 = (uint32_t)h1.x | ((uint32_t)h1.y << 16), w3 = (uint32_t)h1.z | ((uint32_t)h1.w << 16);
       const uint32_t local = smem_addr(hist_all + ((size_t)rank * G + g) * kHistBins + b0);
       for (int r = 0; r < C; ++r)
-        st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), r));
+        if (C == 1) st_shared_v4(local, w0, w1, w2, w3);
+        else st_async_v4(mapa_shared(local, r), w0, w1, w2, w3, mapa_shared(smem_addr(hist_bar), r));
     }
-    mbar_wait(hist_bar, 0);
+    if (C == 1) consumer_sync();
+    else mbar_wait(hist_bar, 0);
     ADAMAS_TRACE(4);
 
     // Head g's T = smallest distance whose cumulative count over all ranks
@@ -900,13 +919,20 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
       const uint32_t local = smem_addr(inbox + ((g / C) * C + rank) * kPartStride);
       const uint32_t dst = mapa_shared(local, (uint32_t)(g % C));
       const uint32_t bar = mapa_shared(smem_addr(inbox_bar), (uint32_t)(g % C));
+      if (C == 1) {  // own inbox (no st.async within a one-CTA "cluster")
+        if (lane == 0) st_shared_v4(local, __float_as_uint(M), __float_as_uint(Lsum), 0u, 0u);
+        st_shared_v4(local + 16 + lane * 16, __float_as_uint(acc[0]), __float_as_uint(acc[1]),
+                     __float_as_uint(acc[2]), __float_as_uint(acc[3]));
+      } else {
       if (lane == 0) st_async_v4(dst, __float_as_uint(M), __float_as_uint(Lsum), 0u, 0u, bar);
       st_async_v4(dst + 16 + lane * 16, __float_as_uint(acc[0]), __float_as_uint(acc[1]), __float_as_uint(acc[2]),
                   __float_as_uint(acc[3]), bar);
+      }
     }
   }
   ADAMAS_TRACE(9);
-  if (n_owned) mbar_wait(inbox_bar, 0);  // all C partials of the heads this rank merges
+  if (C == 1) consumer_sync();
+  else if (n_owned) mbar_wait(inbox_bar, 0);  // all C partials of the heads this rank merges
   ADAMAS_TRACE(10);
 
   // ---------------------------------------------------------------- merge

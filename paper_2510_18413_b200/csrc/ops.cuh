@@ -69,9 +69,19 @@ __device__ __forceinline__ Code load_code(const uint4* planes, int64_t cap, int6
 }
 
 // ----------------------------------------------------------------- append
-// One warp per (token, kv-head) vector: copy k and v into the cache rows and
-// write the key's code (encoded here, or converted from reference words).
+// Bulk encode + append (the build_cache loop, sweep.cpp:38-50, and
+// KvCache::update, kv_cache.cpp:62-71). A warp takes a block of kAppendNV
+// consecutive tokens of ONE kv-head: their K/V rows are loaded (one 256-B row
+// per vector for bf16, coalesced), encoded together (independent shuffle
+// chains interleave), written to the head's rows, and their codes land as
+// kAppendNV consecutive 16-B records per plane (lanes 0..NV-1: one coalesced
+// store per plane). The next block's rows are loaded before the current one is
+// encoded, so the HBM latency overlaps the encode.
 constexpr int kAppendWarps = 8;
+#ifndef ADAMAS_APPEND_NV
+#define ADAMAS_APPEND_NV 2  // measured: 2 -> 434 us, 4 -> 465, 8 -> 610 for 32 heads x 32K (bf16)
+#endif
+constexpr int kAppendNV = ADAMAS_APPEND_NV;
 
 template <typename T, bool kCoded>
 __global__ void __launch_bounds__(kAppendWarps * 32)
@@ -80,24 +90,37 @@ append_kernel(const T* __restrict__ keys, const T* __restrict__ values,
               int64_t cap, T* __restrict__ K, T* __restrict__ V, uint4* __restrict__ codes,
               int* __restrict__ status) {
   __shared__ double sq[kAppendWarps][kHeadDim];
+  constexpr int NV = kAppendNV;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // two vectors per warp and iteration: independent shuffle chains interleave
-  constexpr int NV = 2;
-  const int64_t stride = (int64_t)gridDim.x * kAppendWarps * NV;
-  for (int64_t v0 = ((int64_t)blockIdx.x * kAppendWarps + warp) * NV; v0 < n_vec; v0 += stride) {
-    typename Raw4<T>::V kr[NV], vr[NV];
+  const int n_tok = (int)(n_vec / n_kv);                  // < 2^31 (capacity bound)
+  const int nblocks = (n_tok + NV - 1) / NV * n_kv;     // (token block, kv-head) pairs
+  const int stride = gridDim.x * kAppendWarps;
+  using R = typename Raw4<T>::V;
+  auto load = [&](int b, R (&kr)[NV], R (&vr)[NV]) {
+    const int h = b % n_kv;
+    const int64_t t0 = (int64_t)(b / n_kv) * NV;
 #pragma unroll
     for (int n = 0; n < NV; ++n) {
-      const int64_t vec = min(v0 + n, n_vec - 1);
-      kr[n] = Raw4<T>::load(keys + vec * kHeadDim + lane * 4);
-      vr[n] = Raw4<T>::load(values + vec * kHeadDim + lane * 4);
+      const int64_t t = min(t0 + n, (int64_t)n_tok - 1);
+      const int64_t off = (t * n_kv + h) * kHeadDim + lane * 4;
+      kr[n] = Raw4<T>::load(keys + off);
+      vr[n] = Raw4<T>::load(values + off);
     }
+  };
+  R kr[NV], vr[NV], krn[NV], vrn[NV];
+  int b = blockIdx.x * kAppendWarps + warp;
+  if (b < nblocks) load(b, kr, vr);
+  for (; b < nblocks; b += stride) {
+    if (b + stride < nblocks) load(b + stride, krn, vrn);  // the next block is in flight during this one
+    const int h = b % n_kv;
+    const int64_t t0 = (int64_t)(b / n_kv) * NV;
+    const int nv = (int)min((int64_t)NV, (int64_t)n_tok - t0);
     Code c[NV];
     if constexpr (kCoded) {
 #pragma unroll
       for (int n = 0; n < NV; ++n) {
-        const int64_t vec = min(v0 + n, n_vec - 1);
-        planes_from_ref_byte(reinterpret_cast<const uint8_t*>(codes_ref + vec * 16)[lane], c[n]);
+        const int64_t t = min(t0 + n, (int64_t)n_tok - 1);
+        planes_from_ref_byte(reinterpret_cast<const uint8_t*>(codes_ref + (t * n_kv + h) * 16)[lane], c[n]);
       }
     } else {
       float f[NV][4];
@@ -108,20 +131,33 @@ append_kernel(const T* __restrict__ keys, const T* __restrict__ values,
 #pragma unroll
       for (int n = 0; n < NV; ++n) {
         if (res[n] < 0) res[n] = encode128_warp(f[n], sq[warp], c[n], true) ? 1 : 0;  // exact fallback
-        if (res[n] == 0 && lane == 0 && v0 + n < n_vec) atomicOr(status, kStatusDegenerate);
+        if (res[n] == 0 && lane == 0 && n < nv) atomicOr(status, kStatusDegenerate);
       }
     }
+    const int64_t row0 = (int64_t)h * cap + seq0 + t0;
 #pragma unroll
     for (int n = 0; n < NV; ++n) {
-      const int64_t vec = v0 + n;
-      if (vec >= n_vec) break;
-      const int64_t t = vec / n_kv;
-      const int h = (int)(vec % n_kv);
-      const int64_t row = (int64_t)h * cap + seq0 + t;
-      Raw4<T>::store(K + row * kHeadDim + lane * 4, kr[n]);
-      Raw4<T>::store(V + row * kHeadDim + lane * 4, vr[n]);
-      if (lane == 0) store_code(codes + (int64_t)h * 2 * cap, cap, seq0 + t, c[n]);
+      if (n < nv) {
+        Raw4<T>::store(K + (row0 + n) * kHeadDim + lane * 4, kr[n]);
+        Raw4<T>::store(V + (row0 + n) * kHeadDim + lane * 4, vr[n]);
+      }
     }
+    // codes: lane n < nv writes token t0 + n's record in both planes
+    uint4 lo = make_uint4(0, 0, 0, 0), xx = lo;
+#pragma unroll
+    for (int n = 0; n < NV; ++n)
+      if (lane == n) {
+        lo = make_uint4(c[n].lo[0], c[n].lo[1], c[n].lo[2], c[n].lo[3]);
+        xx = make_uint4(c[n].lo[0] ^ c[n].hi[0], c[n].lo[1] ^ c[n].hi[1], c[n].lo[2] ^ c[n].hi[2],
+                        c[n].lo[3] ^ c[n].hi[3]);
+      }
+    if (lane < nv) {
+      uint4* planes = codes + (int64_t)h * 2 * cap;
+      planes[seq0 + t0 + lane] = lo;
+      planes[cap + seq0 + t0 + lane] = xx;
+    }
+#pragma unroll
+    for (int n = 0; n < NV; ++n) { kr[n] = krn[n]; vr[n] = vrn[n]; }
   }
 }
 
@@ -486,16 +522,15 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   extern __shared__ uint32_t skeys[];  // the n_ranks * budget keys of this q-head, read once
   __shared__ int hist[kSelBins];
   __shared__ int scratch[32];
-  __shared__ int s_T, s_below, n_ties, n_surv, n_local;
-  __shared__ int ties[kSelMaxKeys / 4];
-  __shared__ int surv[kSelMaxSurv];
-  __shared__ int local_rows[kSelMaxSurv];
+  __shared__ int s_T, s_below, s_rem, s_bad;
+  __shared__ uint32_t s_pre;
+  __shared__ int rows[kSelMaxSurv];  // this rank's survivors (local rows), ascending
   __shared__ float wm[kSelThreads / 32], wl[kSelThreads / 32];
   __shared__ float wo[kSelThreads / 32][kHeadDim];
   const int h = blockIdx.x, hk = h / group;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = n_ranks * (int)budget;
-  auto key_at = [&](int j) { return skeys[j]; };  // j = r * budget + i
+  constexpr uint32_t kEmpty = 0xffffffffu;
   // programmatic dependent launch: keys / the appended row come from the
   // preceding kernel; the next launch may begin its own prologue now
   grid_dependency_wait();
@@ -505,7 +540,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   if (tid == 0 && merge_out == nullptr) grid_launch_dependents();
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
   if (tid == 0) {
-    n_ties = 0; n_surv = 0; n_local = 0; s_T = -1; s_below = 0;
+    s_T = -1; s_below = 0; s_bad = 0;
     if (push.n) peer_wait(wait_flags, n_ranks, push.epoch, status);  // every rank's keys of this step have landed
   }
   __syncthreads();
@@ -513,9 +548,19 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     const int r = j / (int)budget, i = j - r * (int)budget;
     const uint32_t key = ld_mailbox(keys + ((int64_t)r * n_q + h) * budget + i);
     skeys[j] = key;
-    if (key != 0xffffffffu) atomicAdd(&hist[key >> 23], 1);
+    if (key != kEmpty) atomicAdd(&hist[key >> 23], 1);
   }
   __syncthreads();
+  // Input contract (adamas_seq_local_candidates): each rank's keys ascending
+  // in the index field, empty keys last; ranks in sequence order. The array
+  // is then ascending in index, so an order-preserving compaction emits the
+  // selection in top_k's output order without a sort.
+  for (int j = tid; j + 1 < n; j += kSelThreads) {
+    if ((j + 1) % (int)budget == 0) continue;  // the next key belongs to the next rank
+    const uint32_t a = skeys[j], b = skeys[j + 1];
+    if ((a == kEmpty && b != kEmpty) || (a != kEmpty && b != kEmpty && (a & 0x7fffffu) >= (b & 0x7fffffu)))
+      s_bad = 1;
+  }
   {  // T = smallest distance whose cumulative count reaches k_eff (one bin per thread)
     const int v = hist[tid];
     int excl, total;
@@ -523,62 +568,79 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     if (excl < k_eff && excl + v >= k_eff) { s_T = tid; s_below = excl; }
   }
   __syncthreads();
-  const int Tthr = s_T, need = k_eff - s_below;
-  for (int j = tid; j < n; j += kSelThreads) {
-    const uint32_t key = key_at(j);
-    if (key != 0xffffffffu && (int)(key >> 23) == Tthr) {
-      const int t = atomicAdd(&n_ties, 1);
-      if (t < kSelMaxKeys / 4) ties[t] = (int)(key & 0x7fffffu);
-    }
+  if (s_bad) {
+    if (tid == 0) atomicOr(status, kStatusBadSelection);
+    return;  // (the peer-exchange launch's waiters time out on the missing partial and latch it too)
   }
-  __syncthreads();
-  const int nt = min(n_ties, kSelMaxKeys / 4);
-  for (int j = tid; j < n; j += kSelThreads) {
-    const uint32_t key = key_at(j);
-    if (key == 0xffffffffu) continue;
-    const int d = (int)(key >> 23), idx = (int)(key & 0x7fffffu);
-    bool take = d < Tthr;
-    if (d == Tthr) {  // ties resolve toward lower indices
-      int r = 0;
-      if (n_ties <= kSelMaxKeys / 4) {
-        for (int t = 0; t < nt; ++t) r += ties[t] < idx;
-      } else {  // more ties than the list holds: rank against every key
-        for (int j2 = 0; j2 < n; ++j2) {
-          const uint32_t k2 = key_at(j2);
-          r += k2 != 0xffffffffu && (int)(k2 >> 23) == Tthr && (int)(k2 & 0x7fffffu) < idx;
-        }
+  // Keys are unique (dist << 23 | global index), ordered like top_k's (score,
+  // index): the selection is every key <= K*, the k_eff-th smallest. Its
+  // distance field is T; its index is the need-th smallest index among the
+  // keys at T, found by a radix select over the 23 index bits (8 + 8 + 7).
+  const int Tthr = s_T;
+  if (tid == 0) { s_pre = 0u; s_rem = k_eff - s_below; }
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = pass == 0 ? 15 : (pass == 1 ? 7 : 0);
+    const int width = pass == 2 ? 7 : 8;
+    __syncthreads();
+    for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
+    __syncthreads();
+    const uint32_t pre = s_pre;
+    const uint32_t hi_mask = 0x7fffffu & ~((1u << (shift + width)) - 1u);
+    for (int j = tid; j < n; j += kSelThreads) {
+      const uint32_t key = skeys[j];
+      if (key != kEmpty && (int)(key >> 23) == Tthr && (key & hi_mask) == pre)
+        atomicAdd(&hist[(key >> shift) & ((1u << width) - 1u)], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {  // the digit whose cumulative count reaches the remaining need
+      int c[8], sum = 0;
+#pragma unroll
+      for (int q2 = 0; q2 < 8; ++q2) { c[q2] = hist[lane * 8 + q2]; sum += c[q2]; }
+      int incl = sum;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const int o = __shfl_up_sync(kFull, incl, m);
+        if (lane >= m) incl += o;
       }
-      take = r < need;
-    }
-    if (!take) continue;
-    const int s = atomicAdd(&n_surv, 1);
-    if (s < kSelMaxSurv) surv[s] = idx;
-    if (idx >= rank_base && idx < rank_base + rank_len) {
-      const int l = atomicAdd(&n_local, 1);
-      if (l < kSelMaxSurv) local_rows[l] = idx - (int)rank_base;
+      const int rem = s_rem;
+      int before = incl - sum;
+#pragma unroll
+      for (int q2 = 0; q2 < 8; ++q2) {
+        if (before < rem && before + c[q2] >= rem) {
+          s_pre = pre | ((uint32_t)(lane * 8 + q2) << shift);
+          s_rem = rem - before;
+        }
+        before += c[q2];
+      }
     }
   }
   __syncthreads();
-  const int ns = min(n_surv, kSelMaxSurv), nl = min(n_local, kSelMaxSurv);
-  if (gidx != nullptr) {  // the global selection, ascending (top_k's output order)
-    for (int i = tid; i < ns; i += kSelThreads) {
-      const int idx = surv[i];
-      int r = 0;
-      for (int j = 0; j < ns; ++j) r += surv[j] < idx;
-      gidx[(int64_t)h * budget + r] = idx;
-    }
-    for (int i = ns + tid; i < budget; i += kSelThreads) gidx[(int64_t)h * budget + i] = -1;
+  const uint32_t kstar = ((uint32_t)Tthr << 23) | s_pre;  // the k_eff-th smallest key
+  // order-preserving compaction over contiguous per-thread runs of the array
+  const int per = (n + kSelThreads - 1) / kSelThreads;
+  const int j0 = min(n, tid * per), j1 = min(n, j0 + per);
+  auto is_local = [&](uint32_t key) {
+    const int64_t idx = key & 0x7fffffu;
+    return idx >= rank_base && idx < rank_base + rank_len;
+  };
+  int my_sel = 0, my_loc = 0;
+  for (int j = j0; j < j1; ++j) {
+    const uint32_t key = skeys[j];
+    if (key <= kstar) { ++my_sel; my_loc += is_local(key); }
   }
-  // this rank's survivors in ascending order (the atomics above collect them in
-  // arbitrary order; a fixed order makes the fp32 attention deterministic)
-  __syncthreads();
-  int* rows = ties;  // the tie list is no longer needed; nl <= kSelMaxSurv == kSelMaxKeys / 4
-  for (int i = tid; i < nl; i += kSelThreads) {
-    const int v = local_rows[i];
-    int r = 0;
-    for (int j = 0; j < nl; ++j) r += local_rows[j] < v;
-    rows[r] = v;
+  int sel_before, sel_total, loc_before, nl;
+  sel_block_excl_scan(my_sel, sel_before, sel_total, scratch);
+  sel_block_excl_scan(my_loc, loc_before, nl, scratch);
+  for (int j = j0; j < j1; ++j) {
+    const uint32_t key = skeys[j];
+    if (key > kstar) continue;
+    const int idx = (int)(key & 0x7fffffu);
+    if (gidx != nullptr) gidx[(int64_t)h * budget + sel_before] = idx;  // the global selection, ascending
+    ++sel_before;
+    if (is_local(key)) rows[loc_before++] = idx - (int)rank_base;
   }
+  if (gidx != nullptr)
+    for (int i = k_eff + tid; i < budget; i += kSelThreads) gidx[(int64_t)h * budget + i] = -1;
   __syncthreads();
   // attention over this rank's survivors: per-warp online softmax, log2 units
   float qf[4];

@@ -54,27 +54,27 @@ class CudaSeqOps:
     def __init__(self):
         self.L = load()
 
-    def local_candidates(self, cache, q, k_new, v_new, append: bool, base: int, budget: int, stream=None):
+    def local_candidates(self, cache, q, k_new, v_new, append: bool, base: int, budget: int, stream=None, out=None):
         n_q = q.numel() // HEAD_DIM
-        keys = torch.empty((n_q, budget), dtype=torch.int32, device=q.device)  # uint32 bit patterns
+        keys = out if out is not None else torch.empty((n_q, budget), dtype=torch.int32, device=q.device)  # u32 bits
         check(self.L.adamas_seq_local_candidates(cache.h, _ptr(q), n_q, _ptr(k_new if append else None),
                                                  _ptr(v_new if append else None), int(append), base, budget,
                                                  _ptr(keys), _stream(stream)))
         return keys
 
     def select_attend(self, cache, q, gathered, budget: int, total_len: int, base: int, want_idx=False,
-                      stream=None):
+                      stream=None, out=None):
         n_q = q.numel() // HEAD_DIM
         world = gathered.shape[0]
-        partial = torch.empty((n_q, PARTIAL_STRIDE), dtype=torch.float32, device=q.device)
+        partial = out if out is not None else torch.empty((n_q, PARTIAL_STRIDE), dtype=torch.float32, device=q.device)
         gidx = torch.empty((n_q, budget), dtype=torch.int32, device=q.device) if want_idx else None
         check(self.L.adamas_seq_select_attend(cache.h, _ptr(q), n_q, _ptr(gathered.contiguous()), world, budget,
                                               total_len, base, _ptr(partial), _ptr(gidx), _stream(stream)))
         return partial, gidx
 
-    def lse_merge(self, partials, stream=None):
+    def lse_merge(self, partials, stream=None, out=None):
         world, n_q = partials.shape[0], partials.shape[1]
-        out = torch.empty((n_q, HEAD_DIM), dtype=torch.float32, device=partials.device)
+        out = out if out is not None else torch.empty((n_q, HEAD_DIM), dtype=torch.float32, device=partials.device)
         check(self.L.adamas_lse_merge(_ptr(partials.contiguous()), world, n_q, _ptr(out), _stream(stream)))
         return out
 

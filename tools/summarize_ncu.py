@@ -152,8 +152,10 @@ def main():
     ap.add_argument("--rep", default=os.path.join(ROOT, "gpurun_out", "prof_fused.ncu-rep"))
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
     ap.add_argument("--name", default="fused")
+    ap.add_argument("--out-dir", default=os.path.join(ROOT, "profiles"),
+                    help="where the summaries go (on a GPU box: under gpurun_out/, merged back)")
     a = ap.parse_args()
-    prof = os.path.join(ROOT, "profiles")
+    prof = a.out_dir
     os.makedirs(prof, exist_ok=True)
     if os.path.exists(a.launches):
         launches(a.launches, os.path.join(prof, f"{a.tag}_launches.txt"))
