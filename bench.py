@@ -440,6 +440,18 @@ def run_ours(args):
                 parity = {"status": "MISMATCH", "detail": f"on rank {int(bad[0]) - 1}"}
             elif parity["status"] == "ok":
                 parity["checked"] += f"; every one of the {ws} ranks checked its own heads"
+    # Isolated latency: the same timed graph with programmatic dependent launch
+    # off, so no launch overlaps its predecessor (what a layer costs when other
+    # kernels sit between attention layers and none of them releases it early).
+    isolated = None
+    if not seqshard:
+        saved_tuning = ad.get_tuning()
+        ad.set_tuning(no_pdl=1)
+        n_iso = min(args.steps, 10)
+        iso_ms, _ = _timed_graph(torch, dist, ws, lambda s, st: step(args.warmup + s, st), n_iso, local)
+        ad.set_tuning(**saved_tuning)
+        isolated = {"value": iso_ms * 1000.0 / (n_iso * L * NS), "unit": UNIT,
+                    "note": "same steps with programmatic dependent launch off: no layer overlaps its predecessor"}
     launches_per_step = L * (3 if seqshard else 1)
     ms_per_step = elapsed_ms / args.steps
     tokens_per_layer = NS  # one decoded token per sequence per layer
@@ -563,6 +575,7 @@ def run_ours(args):
             "clocks": clocks,
             "cpu_baseline": cpu,
             "parity": parity,
+            "isolated": isolated,
         }
         print(json.dumps(line))
         if parity and parity["status"] != "ok":

@@ -167,6 +167,7 @@ int adamas_sparse_attention(const adamas_cache* cache, const void* q, int n_q_he
 int adamas_decode_step(adamas_cache* cache, const void* q, int n_q_heads, const void* k_new,
                        const void* v_new, int64_t budget, float* out, int32_t* idx, void* stream);
 
+
 /* Same step for a batch of independent sequences (per-request caches with the
  * same shape and dtype) in one launch: caches[i], q + i*n_q_heads*128, ...
  * out + i*n_q_heads*128, idx + i*n_q_heads*budget. */

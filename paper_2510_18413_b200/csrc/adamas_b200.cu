@@ -952,8 +952,7 @@ int adamas_sparse_attention(const adamas_cache* c, const void* q, int n_q, const
 
 int adamas_decode_step_batched(adamas_cache* const* caches, int n_seqs, const void* q, int n_q,
                                const void* k_new, const void* v_new, int64_t budget, float* out, int32_t* idx,
-                               void* stream) {
-  if (!caches || n_seqs < 1) return fail(ADAMAS_ERR_CONFIG, "decode: no caches");
+                               void* stream) {  if (!caches || n_seqs < 1) return fail(ADAMAS_ERR_CONFIG, "decode: no caches");
   adamas_cache* c0 = caches[0];
   if (int rc = check_cache(c0)) return rc;
   if (int rc = check_heads(c0, n_q)) return rc;

@@ -37,8 +37,8 @@ namespace adamas_dev {
 #ifndef ADAMAS_DIAG
 #define ADAMAS_DIAG 0  // 1: phase stamps and timing-only switches (ADAMAS_DBG) compiled in (build.py --diag)
 #endif
-#ifndef ADAMAS_L2PF
-#define ADAMAS_L2PF 0  // experiments: 1 = L2 bulk prefetch of the rank's clean codes beyond the ring at CTA start
+#ifndef ADAMAS_QPF
+#define ADAMAS_QPF 1  // L2-prefetch q / k_new / v_new before the grid-dependency wait
 #endif
 #ifndef ADAMAS_GATHER_PREFETCH
 #define ADAMAS_GATHER_PREFETCH 2  // L2-prefetch the gather rows: 1 all rows <= T in the count pass, 2 survivors in the emit, 0 none
@@ -386,14 +386,6 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     mbar_init(sc_bar, 1);
     mbar_fence_init();
     for (int st = 0; st < min(ring, n_stages); ++st) issue(st, st);
-    if (ADAMAS_L2PF) {  // the rest of the clean range toward L2 while the launch waits for its predecessor
-      for (int st = ring; st < n_stages; ++st) {
-        const int ntok = min(kStageTok, clean_local - st * kStageTok);
-        if (ntok <= 0) break;
-        bulk_prefetch_l2(lo_g + (int64_t)st * kStageTok, (uint32_t)ntok * 16u);
-        bulk_prefetch_l2(x_g + (int64_t)st * kStageTok, (uint32_t)ntok * 16u);
-      }
-    }
     // bytes this CTA will receive over DSMEM: every rank's u16 histograms, and
     // C partials per q-head it merges
     // (a single-CTA unit exchanges through its own shared memory: plain stores
@@ -408,6 +400,20 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   float f[4] = {0.f, 0.f, 0.f, 0.f};
   typename Raw4<T>::V kr{}, vr{};
   if (p.pdl && warp <= G) {
+#if ADAMAS_QPF
+    // warm L2 with this unit's q / k_new / v_new lines while the predecessor
+    // runs: the reads after the wait then hit L2 (a prefetch of a line the
+    // predecessor is still writing is harmless, L2 is the coherence point)
+    if (lane < 2) {
+      if (warp < G)
+        prefetch_l2(reinterpret_cast<const char*>(reinterpret_cast<const T*>(p.q) + ((int64_t)si * n_q + q0 + warp) * kHeadDim) + lane * 128);
+      else if (has_new) {
+        const int64_t vrow = (int64_t)si * p.n_kv + hk;
+        prefetch_l2(reinterpret_cast<const char*>(reinterpret_cast<const T*>(p.k_new) + vrow * kHeadDim) + lane * 128);
+        prefetch_l2(reinterpret_cast<const char*>(reinterpret_cast<const T*>(p.v_new) + vrow * kHeadDim) + lane * 128);
+      }
+    }
+#endif
     // q, k_new, v_new and the cache tail come from preceding kernels. Once the
     // predecessor has completed, the next launch may start its prologue.
     grid_dependency_wait();
@@ -450,14 +456,12 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   if (warp < G) {  // encode query head hk * G + warp (sweep.cpp:92-94)
     *reinterpret_cast<float4*>(qfs + warp * kHeadDim + lane * 4) = make_float4(f[0], f[1], f[2], f[3]);
     Code c;
-    ADAMAS_TRACE(12);
     if (pdbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
       for (int w = 0; w < 4; ++w) { c.lo[w] = __float_as_uint(f[w]); c.hi[w] = 0u; }
       if (lane == 0) qcode[warp] = c;
     } else if (!encode128_to(f, sqs + warp * kHeadDim, qcode + warp, p.exact_encode != 0) && lane == 0) {
       atomicOr(p.seq[si].status, kStatusDegenerate);
     }
-    ADAMAS_TRACE(13);
   } else if (has_new && warp == G) {  // append (kv_cache.cpp:62-71); part 0 of a split kv-head writes
     const int64_t row = (int64_t)hk * cap + s_old;
     if (part == 0) {
@@ -546,6 +550,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   }
   consumer_sync();  // local histogram final
   ADAMAS_TRACE(3);
+  if (ADAMAS_DIAG && (pdbg & (1 << 16))) return;  // diagnostics (timing only): stop after the scan
   const int k_eff = (int)min((int64_t)p.budget, S);
   const int g_me = tid / NT, t_in = tid % NT;
   cluster_wait();
@@ -681,6 +686,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   }
   consumer_sync();
   ADAMAS_TRACE(5);
+  if (ADAMAS_DIAG && (pdbg & (1 << 17))) return;  // diagnostics (timing only): stop once T is known
 
   // ---------------------------------------------------------------- compaction
   // Thread t_in of head g owns a contiguous span of tokens: count (< T, == T)
@@ -759,6 +765,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
           prefetch_row(grp * 32 + __ffs(m) - 1);
       }
     }
+    ADAMAS_TRACE(12);
     int lt_before, eq_before, lt_tot, eq_tot;
     head_scan2<G>(my_lt, my_eq, lt_before, eq_before, lt_tot, eq_tot, scratch);
     if (t_in == 0) nsel[g] = min(lt_tot + min(eq_tot, eq_budget), selcap);
@@ -806,6 +813,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
         }
       }
     }
+    ADAMAS_TRACE(13);
     if (gr == 0 && p.idx && t_in == 0) {  // estimator.cpp:80 caps the selection at S
       int32_t* row = p.idx + ((int64_t)si * n_q + q0 + g) * p.budget;
       for (int i = k_eff; i < p.budget; ++i) row[i] = -1;
@@ -822,6 +830,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   }
   consumer_sync();
   ADAMAS_TRACE(7);
+  if (ADAMAS_DIAG && (pdbg & (1 << 19))) return;  // diagnostics (timing only): stop after the compaction
   if (pcand) {  // candidates mode: the selection is the product
     if (p.peers.n && tid == 0) peer_signal(p.peers);
     return;
@@ -830,7 +839,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   // ---------------------------------------------------------------- attend
   {
     const int g = warp % G, sub = warp / G;
-    const int ns = nsel[g];
+    const int ns = (ADAMAS_DIAG && (pdbg & (1 << 18))) ? 0 : nsel[g];  // diagnostics: no gather
     const float4 q4 = *reinterpret_cast<const float4*>(qfs + g * kHeadDim + lane * 4);
     float qf[4] = {q4.x, q4.y, q4.z, q4.w};
     const float scale = 0.088388347648318440f * kLog2e;  // 1/sqrt(128), log2 units

@@ -112,8 +112,8 @@ for i in range(1, 12):
     d = cum.mean() - prev.mean()
     print(f"{names[i]:42s} {cum.mean():9.2f} {cum.max():9.2f} {d:7.2f}   (graph {us_i:.2f} us/layer)")
     prev = cum
-for i in (12, 13):
+for i, what in ((12, "compaction masks done (before the prefix)"), (13, "emit done (before the -1 fill)")):
     us_i, ti = timed_graph(i)
     cum = (ti[:, i] - ti[:, 14]) / 1000.0
-    print(f"stamp {i}: cum mean {cum.mean():.2f} max {cum.max():.2f}")
+    print(f"stamp {i} {what}: cum mean {cum.mean():.2f} max {cum.max():.2f}")
 ad.set_tuning(dbg=base_dbg)
