@@ -31,7 +31,7 @@ ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--budget", type=int, default=128)
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--cluster", default="")
-ap.add_argument("--traced", type=int, default=-1, help="index of the traced layer")
+ap.add_argument("--traced", type=int, default=-2, help="index of the traced layer")
 ap.add_argument("--seqs", type=int, default=1, help="independent sequences per launch (batched decode)")
 args = ap.parse_args()
 if args.cluster:
@@ -55,16 +55,20 @@ for _ in range(args.layers):
 q = torch.randn((args.seqs, args.heads, 128), generator=gen, device="cuda").bfloat16()
 k = torch.randn((args.seqs, args.kv_heads, 128), generator=gen, device="cuda").bfloat16()
 trace = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+trace_prev = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")  # launch before the traced one (start/end)
 names = ["start", "prologue (zero, q load, barrier init)", "encode + append", "scan", "hist exchange",
          "threshold", "compact count (+L2 prefetch) + scan", "compact emit",
          "attend gather", "attend combine + push", "inbox wait", "merge"]
+prev_end = None
 base_dbg = int(os.environ.get("ADAMAS_DBG", "0")) & 0xff
 
 
 def run_layers():
     for li, per in enumerate(caches):
         traced = li == (args.traced % len(caches))
-        L.adamas_debug_trace(C.c_void_p(trace.data_ptr()) if traced else None)
+        before = li == (args.traced % len(caches)) - 1
+        buf = trace if traced else (trace_prev if before else None)
+        L.adamas_debug_trace(C.c_void_p(buf.data_ptr()) if buf is not None else None)
         if args.seqs == 1:
             per[0].decode_step(q[0], k[0], k[0], args.budget)
         else:
@@ -77,6 +81,7 @@ def run_layers():
 def timed_graph(stamp):
     ad.set_tuning(dbg=base_dbg | ((stamp + 1) << 8 if stamp >= 0 else 0))
     trace.zero_()
+    trace_prev.zero_()
     run_layers()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -93,8 +98,12 @@ def timed_graph(stamp):
     t = trace.view(-1, 16).cpu()
     n = int((t[:, 14] > 0).sum())
     t = t[:n].double()
+    tp = trace_prev.view(-1, 16).cpu()
+    tp = tp[: int((tp[:, 14] > 0).sum())].double()
     if not (base_dbg & 64):  # clock64 stamps -> ns
         t = t / float(os.environ.get("SM_GHZ", "1.965"))
+    global prev_end
+    prev_end = float(tp[:, 15].max()) if (base_dbg & 64) and tp.shape[0] else None
     return e0.elapsed_time(e1) * 1000 / len(caches), t
 
 
@@ -105,15 +114,27 @@ print(f"graph: {us:.2f} us per layer; traced launch: {t.shape[0]} CTAs, per-CTA 
                                  f" -> last end {(t[:, 15].max() - t[:, 14].min()) / 1000:.2f} us"
                                  if base_dbg & 64 else " (clock64 stamps; ADAMAS_DBG=64 for globaltimer)"))
 prev = torch.zeros(t.shape[0], dtype=torch.float64)
+if prev_end is not None:  # globaltimer: the critical path, from the previous launch's last CTA end
+    print(f"traced launch vs the previous launch's last CTA end: first CTA start {(t[:, 14].min() - prev_end) / 1000:+.2f} us, "
+          f"last CTA end {(t[:, 15].max() - prev_end) / 1000:+.2f} us, CTA end spread {(t[:, 15].max() - t[:, 15].min()) / 1000:.2f} us")
+    print(f"{'phase (ends at stamp), since prev end':42s} {'mean':>8s} {'min':>8s} {'max':>8s}")
 print(f"{'phase (ends at stamp)':42s} {'cum mean':>9s} {'cum max':>9s} {'delta':>7s}")
 for i in range(1, 12):
     us_i, ti = timed_graph(i)
+    if prev_end is not None:
+        rel = (ti[:, i] - prev_end) / 1000.0
+        print(f"{names[i]:42s} {rel.mean():8.2f} {rel.min():8.2f} {rel.max():8.2f}   (graph {us_i:.2f} us/layer)")
+        continue
     cum = (ti[:, i] - ti[:, 14]) / 1000.0
     d = cum.mean() - prev.mean()
     print(f"{names[i]:42s} {cum.mean():9.2f} {cum.max():9.2f} {d:7.2f}   (graph {us_i:.2f} us/layer)")
     prev = cum
 for i, what in ((12, "compaction masks done (before the prefix)"), (13, "emit done (before the -1 fill)")):
     us_i, ti = timed_graph(i)
+    if prev_end is not None:
+        rel = (ti[:, i] - prev_end) / 1000.0
+        print(f"stamp {i} {what}: since prev end mean {rel.mean():.2f} max {rel.max():.2f}")
+        continue
     cum = (ti[:, i] - ti[:, 14]) / 1000.0
     print(f"stamp {i} {what}: cum mean {cum.mean():.2f} max {cum.max():.2f}")
 ad.set_tuning(dbg=base_dbg)
