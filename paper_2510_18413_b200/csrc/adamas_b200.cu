@@ -113,10 +113,17 @@ int launch_append(adamas_cache* c, const void* keys, const void* values, const u
     append_kernel<T, true><<<grid, kAppendWarps * 32, 0, s>>>(
         (const T*)keys, (const T*)values, codes_ref, n_vec, c->n_kv, c->seq_len, c->capacity, (T*)c->K,
         (T*)c->V, c->codes, c->status);
-  else
+  else if (n_vec < 4 * kAppend8Warps)  // a few vectors: the 2-per-warp kernel, no idle groups
     append_kernel<T, false><<<grid, kAppendWarps * 32, 0, s>>>(
         (const T*)keys, (const T*)values, nullptr, n_vec, c->n_kv, c->seq_len, c->capacity, (T*)c->K,
         (T*)c->V, c->codes, c->status);
+  else {  // bulk: four vectors per warp through the 8-lane encoder
+    const int64_t blocks8 = (n_vec + 4 * kAppend8Warps - 1) / (4 * kAppend8Warps);
+    const int grid8 = (int)std::min<int64_t>(blocks8, (int64_t)sm_count() * 8);
+    append8_kernel<T><<<grid8, kAppend8Warps * 32, 0, s>>>((const T*)keys, (const T*)values, n_vec, c->n_kv,
+                                                           c->seq_len, c->capacity, (T*)c->K, (T*)c->V, c->codes,
+                                                           c->status);
+  }
   return launch_check("append_kernel");
 }
 
@@ -241,6 +248,8 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
     if (kf.smem_configured < smem) {
       ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      // all of the unified L1/shared array as shared memory: two CTAs per SM need it
+      ADAMAS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kf.smem_configured = smem;
     }
     if (prm.pdl || prm.P > 1) {

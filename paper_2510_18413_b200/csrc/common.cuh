@@ -374,6 +374,84 @@ __device__ __forceinline__ int encode128_warp_f32(const float in[4], Code& out) 
   return r[0];
 }
 
+// Throughput form of the certified fp32 route, for bulk encodes (prefill):
+// a warp encodes FOUR vectors at once, lanes 8g .. 8g+7 holding vector g,
+// lane L of a group the 16 consecutive elements 16L .. 16L+15. The first
+// four butterfly stages are in-register, only three cross lanes (instead of
+// five at 4 elements per lane), and the network is left unnormalized:
+// Y = sqrt(128) y exactly in real arithmetic, and y > t  <=>  Y > kQ28 ||x||,
+// so no per-stage multiply is needed. Rounding bound (u = 2^-24): a stage-s
+// node holds a sum of 2^s inputs, |v| <= 2^(s/2) ||x||, and reaches an output
+// through 2^(7-s) ancestors, so |Y - Y_exact| <= u ||x|| sum_s 2^(7 - s/2)
+// = 282 u ||x|| = 1.7e-5 sigma in y units; the fp32 sum of squares and the
+// square root put the threshold within ~2.6e-6 sigma; the reference's fp64
+// values are within ~1e-14 sigma. A code is certain when Y is farther than
+// E = 2^-15 ||x|| (= 3.05e-5 sigma in y units, 1.6x the total) from every
+// threshold. Out (uniform within a group): res 1 certain / -1 not certified
+// (also for sums of squares outside [1e-30, 1e37]: the exact path decides,
+// including degenerate vectors); `out` = the group's code in every lane.
+__device__ __forceinline__ int encode128_g8_f32(const float (&in)[16], Code& out) {
+  const int lane = threadIdx.x & 31, L = lane & 7;
+  float v[16];
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = in[i];
+    sq = __fmaf_rn(v[i], v[i], sq);
+  }
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i & h) continue;
+      const float a = v[i], b = v[i + h];
+      v[i] = __fadd_rn(a, b);
+      v[i + h] = __fsub_rn(a, b);
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < 8; m <<= 1) {
+    const float sgn = (L & m) ? -1.f : 1.f;  // lower: a + b; upper: a - b (a = the partner's)
+    sq = __fadd_rn(sq, __shfl_xor_sync(kFull, sq, m));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __fmaf_rn(sgn, v[i], __shfl_xor_sync(kFull, v[i], m));
+  }
+  const float S = __fsqrt_rn(sq);  // ||x||
+  const float Tq = __fmul_rn(0.6744897501960817432f, S);
+  const float E = S * 3.0517578125e-5f;
+  bool unsure = !(sq > 1e-30f && sq < 1e37f);
+  uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float y = v[i], ay = fabsf(y);
+    unsure |= ay <= E || fabsf(ay - Tq) <= E;
+    const uint32_t c = (uint32_t)(y > -Tq) + (uint32_t)(y > 0.f) + (uint32_t)(y > Tq);
+    // element 16 L + i: word i % 4, bit 4 L + i / 4
+    lo[i & 3] |= (c & 1u) << (i >> 2);
+    hi[i & 3] |= (c >> 1) << (i >> 2);
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    lo[w] <<= 4 * L;
+    hi[w] <<= 4 * L;
+  }
+#pragma unroll
+  for (int m = 1; m < 8; m <<= 1) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      lo[w] |= __shfl_xor_sync(kFull, lo[w], m);
+      hi[w] |= __shfl_xor_sync(kFull, hi[w], m);
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    out.lo[w] = lo[w];
+    out.hi[w] = hi[w];
+  }
+  const unsigned grp = 0xffu << (lane & 24);
+  return (__ballot_sync(kFull, unsure) & grp) ? -1 : 1;
+}
+
 // The encoder used on the hot paths: certified fp32, exact fp64 fallback.
 // exact = true forces the fp64 path (diagnostics / tests).
 __device__ __forceinline__ bool encode128(const float in[4], double* sq, Code& out, bool exact = false) {

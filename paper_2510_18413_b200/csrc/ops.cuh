@@ -161,6 +161,111 @@ append_kernel(const T* __restrict__ keys, const T* __restrict__ values,
   }
 }
 
+// Sixteen consecutive elements (one lane's share of a vector in the 8-lane
+// layout) as raw registers: 32 B (bf16) or 64 B (fp32).
+template <typename T>
+struct Raw16;
+template <>
+struct Raw16<__nv_bfloat16> {
+  uint4 r[2];
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) {
+    r[0] = __ldcs(reinterpret_cast<const uint4*>(p));
+    r[1] = __ldcs(reinterpret_cast<const uint4*>(p) + 1);
+  }
+  __device__ __forceinline__ void store(__nv_bfloat16* p) const {
+    reinterpret_cast<uint4*>(p)[0] = r[0];
+    reinterpret_cast<uint4*>(p)[1] = r[1];
+  }
+  __device__ __forceinline__ void to_float(float (&f)[16]) const {
+    const uint32_t w[8] = {r[0].x, r[0].y, r[0].z, r[0].w, r[1].x, r[1].y, r[1].z, r[1].w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <>
+struct Raw16<float> {
+  float4 r[4];
+  __device__ __forceinline__ void load(const float* p) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = __ldcs(reinterpret_cast<const float4*>(p) + i);
+  }
+  __device__ __forceinline__ void store(float* p) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) reinterpret_cast<float4*>(p)[i] = r[i];
+  }
+  __device__ __forceinline__ void to_float(float (&f)[16]) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[4 * i] = r[i].x; f[4 * i + 1] = r[i].y; f[4 * i + 2] = r[i].z; f[4 * i + 3] = r[i].w;
+    }
+  }
+};
+
+// Bulk prefill (kv_cache.cpp:62-71 per vector, sweep.cpp:38-50's build loop):
+// each warp encodes four consecutive input vectors per iteration through the
+// 8-lane certified encoder (encode128_g8_f32: about half the instructions of
+// the 32-lane route per vector, which made append_kernel issue-bound), copies
+// their K / V rows into the cache and stores the codes; a group whose vector
+// misses the certificate is re-encoded exactly by the whole warp. The next
+// iteration's rows are loaded before this one is encoded.
+constexpr int kAppend8Warps = 8;
+template <typename T>
+__global__ void __launch_bounds__(kAppend8Warps * 32)
+append8_kernel(const T* __restrict__ keys, const T* __restrict__ values, int64_t n_vec, int n_kv, int64_t seq0,
+               int64_t cap, T* __restrict__ K, T* __restrict__ V, uint4* __restrict__ codes,
+               int* __restrict__ status) {
+  __shared__ double sq[kAppend8Warps][kHeadDim];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = lane >> 3, L = lane & 7;
+  const int64_t stride = (int64_t)gridDim.x * kAppend8Warps * 4;
+  int64_t b0 = ((int64_t)blockIdx.x * kAppend8Warps + warp) * 4;  // this warp's first vector
+  Raw16<T> kr, vr, krn, vrn;
+  auto load = [&](int64_t first, Raw16<T>& k, Raw16<T>& v) {
+    const int64_t b = min(first + grp, n_vec - 1);
+    k.load(keys + b * kHeadDim + L * 16);
+    v.load(values + b * kHeadDim + L * 16);
+  };
+  if (b0 < n_vec) load(b0, kr, vr);
+  for (; b0 < n_vec; b0 += stride) {
+    if (b0 + stride < n_vec) load(b0 + stride, krn, vrn);
+    const int64_t b = b0 + grp;
+    const bool valid = b < n_vec;
+    const int64_t t = n_vec <= 0x7fffffff ? (int64_t)((uint32_t)b / (uint32_t)n_kv) : b / n_kv;
+    const int h = (int)(b - t * n_kv);
+    float f[16];
+    kr.to_float(f);
+    Code c;
+    const int res = encode128_g8_f32(f, c);
+    const int64_t row = (int64_t)h * cap + seq0 + t;
+    if (valid) {
+      kr.store(K + row * kHeadDim + L * 16);
+      vr.store(V + row * kHeadDim + L * 16);
+    }
+    uint4* planes = codes + (int64_t)h * 2 * cap;
+    if (valid && res > 0 && L == 0) store_code(planes, cap, seq0 + t, c);
+    // exact path (reference order, fp64) for vectors outside the certificate,
+    // one at a time by the whole warp in the 4-elements-per-lane layout
+    unsigned unsure = __ballot_sync(kFull, valid && res < 0 && L == 0);
+    while (unsure) {
+      const int g = (__ffs(unsure) - 1) >> 3;
+      unsure &= unsure - 1;
+      const int64_t bg = b0 + g;
+      float e[4];
+      Raw4<T>::to_float(Raw4<T>::load(keys + bg * kHeadDim + lane * 4), e);
+      Code ce;
+      const bool ok = encode128_warp(e, sq[warp], ce, true);
+      if (lane == 0) {
+        if (!ok) atomicOr(status, kStatusDegenerate);
+        store_code(codes + (int64_t)(bg % n_kv) * 2 * cap, cap, seq0 + bg / n_kv, ce);
+      }
+    }
+    kr = krn;
+    vr = vrn;
+  }
+}
+
 // ----------------------------------------------------------------- query encode
 template <typename T>
 __global__ void __launch_bounds__(kAppendWarps * 32)
@@ -355,6 +460,7 @@ topk_kernel(const int32_t* __restrict__ scores, int64_t n, int64_t k, int32_t* _
         if (lane >= m) incl += o;
       }
       const int need = s_need;
+      __syncwarp();  // every lane has read s_need before one lane rewrites it (racecheck)
       unsigned before = incl - sum;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -522,8 +628,8 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   extern __shared__ uint32_t skeys[];  // the n_ranks * budget keys of this q-head, read once
   __shared__ int hist[kSelBins];
   __shared__ int scratch[32];
-  __shared__ int s_T, s_below, s_rem, s_bad;
-  __shared__ uint32_t s_pre;
+  __shared__ int s_T, s_below, s_bad;
+  __shared__ int s_lo_cnt, s_in_cnt;  // packed (lt | eq << 16) counts below / inside the local range
   __shared__ int rows[kSelMaxSurv];  // this rank's survivors (local rows), ascending
   __shared__ float wm[kSelThreads / 32], wl[kSelThreads / 32];
   __shared__ float wo[kSelThreads / 32][kHeadDim];
@@ -543,23 +649,48 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     s_T = -1; s_below = 0; s_bad = 0;
     if (push.n) peer_wait(wait_flags, n_ranks, push.epoch, status);  // every rank's keys of this step have landed
   }
+  // the q-head's query, consumed by the attention at the end: its load
+  // latency hides behind the selection
+  const typename Raw4<T>::V q_raw = Raw4<T>::load(q + (int64_t)h * kHeadDim + lane * 4);
+  const T* Kh = K + (int64_t)hk * cap * kHeadDim;
+  const T* Vh = V + (int64_t)hk * cap * kHeadDim;
   __syncthreads();
-  for (int j = tid; j < n; j += kSelThreads) {
-    const int r = j / (int)budget, i = j - r * (int)budget;
-    const uint32_t key = ld_mailbox(keys + ((int64_t)r * n_q + h) * budget + i);
-    skeys[j] = key;
-    if (key != kEmpty) atomicAdd(&hist[key >> 23], 1);
+  {
+    int r = tid / (int)budget, i = tid - r * (int)budget;  // j = r * budget + i, advanced without a division
+    for (int j = tid; j < n; j += kSelThreads) {
+      const uint32_t key = ld_mailbox(keys + ((int64_t)r * n_q + h) * budget + i);
+      skeys[j] = key;
+      if (key != kEmpty) {
+        atomicAdd(&hist[key >> 23], 1);
+        // a local candidate: its K / V rows may be gathered below; warm L2
+        // now so the attention after the selection does not wait on HBM
+        const int64_t t = (int64_t)(key & 0x7fffffu) - rank_base;
+        if (t >= 0 && t < rank_len) {
+#pragma unroll
+          for (int c = 0; c < (int)(kHeadDim * sizeof(T)); c += 128) {
+            prefetch_l2(reinterpret_cast<const char*>(Kh + t * kHeadDim) + c);
+            prefetch_l2(reinterpret_cast<const char*>(Vh + t * kHeadDim) + c);
+          }
+        }
+      }
+      for (i += kSelThreads; i >= (int)budget; i -= (int)budget) ++r;
+    }
   }
   __syncthreads();
   // Input contract (adamas_seq_local_candidates): each rank's keys ascending
   // in the index field, empty keys last; ranks in sequence order. The array
   // is then ascending in index, so an order-preserving compaction emits the
   // selection in top_k's output order without a sort.
-  for (int j = tid; j + 1 < n; j += kSelThreads) {
-    if ((j + 1) % (int)budget == 0) continue;  // the next key belongs to the next rank
-    const uint32_t a = skeys[j], b = skeys[j + 1];
-    if ((a == kEmpty && b != kEmpty) || (a != kEmpty && b != kEmpty && (a & 0x7fffffu) >= (b & 0x7fffffu)))
-      s_bad = 1;
+  {
+    int i = tid % (int)budget;  // position within the rank's keys
+    for (int j = tid; j + 1 < n; j += kSelThreads) {
+      if (i + 1 != (int)budget) {  // (the next key belongs to the next rank otherwise)
+        const uint32_t a = skeys[j], b = skeys[j + 1];
+        if ((a == kEmpty && b != kEmpty) || (a != kEmpty && b != kEmpty && (a & 0x7fffffu) >= (b & 0x7fffffu)))
+          s_bad = 1;
+      }
+      for (i += kSelThreads; i >= (int)budget;) i -= (int)budget;
+    }
   }
   {  // T = smallest distance whose cumulative count reaches k_eff (one bin per thread)
     const int v = hist[tid];
@@ -572,87 +703,71 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     if (tid == 0) atomicOr(status, kStatusBadSelection);
     return;  // (the peer-exchange launch's waiters time out on the missing partial and latch it too)
   }
-  // Keys are unique (dist << 23 | global index), ordered like top_k's (score,
-  // index): the selection is every key <= K*, the k_eff-th smallest. Its
-  // distance field is T; its index is the need-th smallest index among the
-  // keys at T, found by a radix select over the 23 index bits (8 + 8 + 7).
+  // Keys are unique (dist << 23 | global index) and the array ascends in the
+  // index field, so the selection -- the k_eff smallest keys in top_k's
+  // (score, index) order -- is every key at distance < T plus the first
+  // rem = k_eff - below keys at distance T in array order: ONE
+  // order-preserving compaction (a packed (lt, eq) block scan), no radix
+  // select over the index bits. The selection lands in `rows` in ascending
+  // index order; this rank's survivors are the contiguous part of it inside
+  // [rank_base, rank_base + rank_len), located from two block counts.
   const int Tthr = s_T;
-  if (tid == 0) { s_pre = 0u; s_rem = k_eff - s_below; }
-  for (int pass = 0; pass < 3; ++pass) {
-    const int shift = pass == 0 ? 15 : (pass == 1 ? 7 : 0);
-    const int width = pass == 2 ? 7 : 8;
-    __syncthreads();
-    for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
-    __syncthreads();
-    const uint32_t pre = s_pre;
-    const uint32_t hi_mask = 0x7fffffu & ~((1u << (shift + width)) - 1u);
-    for (int j = tid; j < n; j += kSelThreads) {
-      const uint32_t key = skeys[j];
-      if (key != kEmpty && (int)(key >> 23) == Tthr && (key & hi_mask) == pre)
-        atomicAdd(&hist[(key >> shift) & ((1u << width) - 1u)], 1);
-    }
-    __syncthreads();
-    if (warp == 0) {  // the digit whose cumulative count reaches the remaining need
-      int c[8], sum = 0;
-#pragma unroll
-      for (int q2 = 0; q2 < 8; ++q2) { c[q2] = hist[lane * 8 + q2]; sum += c[q2]; }
-      int incl = sum;
-#pragma unroll
-      for (int m = 1; m < 32; m <<= 1) {
-        const int o = __shfl_up_sync(kFull, incl, m);
-        if (lane >= m) incl += o;
-      }
-      const int rem = s_rem;
-      int before = incl - sum;
-#pragma unroll
-      for (int q2 = 0; q2 < 8; ++q2) {
-        if (before < rem && before + c[q2] >= rem) {
-          s_pre = pre | ((uint32_t)(lane * 8 + q2) << shift);
-          s_rem = rem - before;
-        }
-        before += c[q2];
-      }
-    }
-  }
+  const int rem = k_eff - s_below;
+  if (tid == 0) { s_lo_cnt = 0; s_in_cnt = 0; }
   __syncthreads();
-  const uint32_t kstar = ((uint32_t)Tthr << 23) | s_pre;  // the k_eff-th smallest key
-  // order-preserving compaction over contiguous per-thread runs of the array
   const int per = (n + kSelThreads - 1) / kSelThreads;
   const int j0 = min(n, tid * per), j1 = min(n, j0 + per);
-  auto is_local = [&](uint32_t key) {
+  int my_lt = 0, my_eq = 0, lt_lo = 0, eq_lo = 0, lt_in = 0, eq_in = 0;
+  for (int j = j0; j < j1; ++j) {
+    const uint32_t key = skeys[j];
+    if (key == kEmpty) continue;
+    const int d = (int)(key >> 23);
     const int64_t idx = key & 0x7fffffu;
-    return idx >= rank_base && idx < rank_base + rank_len;
-  };
-  int my_sel = 0, my_loc = 0;
-  for (int j = j0; j < j1; ++j) {
-    const uint32_t key = skeys[j];
-    if (key <= kstar) { ++my_sel; my_loc += is_local(key); }
+    const bool lt = d < Tthr, eq = d == Tthr;
+    my_lt += lt;
+    my_eq += eq;
+    if (idx < rank_base) { lt_lo += lt; eq_lo += eq; }
+    else if (idx < rank_base + rank_len) { lt_in += lt; eq_in += eq; }
   }
-  int sel_before, sel_total, loc_before, nl;
-  sel_block_excl_scan(my_sel, sel_before, sel_total, scratch);
-  sel_block_excl_scan(my_loc, loc_before, nl, scratch);
+  // block totals of the range counts (no prefix needed): keys below the
+  // local range that are selected = lt_lo + min(rem, eq_lo), likewise inside
+  lt_lo = __reduce_add_sync(kFull, lt_lo | (eq_lo << 16));
+  lt_in = __reduce_add_sync(kFull, lt_in | (eq_in << 16));
+  if (lane == 0) {
+    if (lt_lo) atomicAdd(&s_lo_cnt, lt_lo);
+    if (lt_in) atomicAdd(&s_in_cnt, lt_in);
+  }
+  int packed_before, packed_total;  // counts < 2^13 (n <= kSelMaxKeys): lt | eq << 16 in one scan
+  sel_block_excl_scan(my_lt | (my_eq << 16), packed_before, packed_total, scratch);
+  int lt_before = packed_before & 0xffff, eq_seen = packed_before >> 16;
+  int pos = lt_before + min(eq_seen, rem);
   for (int j = j0; j < j1; ++j) {
     const uint32_t key = skeys[j];
-    if (key > kstar) continue;
+    if (key == kEmpty) continue;
+    const int d = (int)(key >> 23);
+    if (d > Tthr || (d == Tthr && eq_seen++ >= rem)) continue;
     const int idx = (int)(key & 0x7fffffu);
-    if (gidx != nullptr) gidx[(int64_t)h * budget + sel_before] = idx;  // the global selection, ascending
-    ++sel_before;
-    if (is_local(key)) rows[loc_before++] = idx - (int)rank_base;
+    if (gidx != nullptr) gidx[(int64_t)h * budget + pos] = idx;  // the global selection, ascending
+    rows[pos++] = idx;
   }
   if (gidx != nullptr)
     for (int i = k_eff + tid; i < budget; i += kSelThreads) gidx[(int64_t)h * budget + i] = -1;
   __syncthreads();
+  const int lo_cnt = s_lo_cnt, in_cnt = s_in_cnt;
+  const int sel_lo = (lo_cnt & 0xffff) + min(rem, lo_cnt >> 16);  // selected below the local range
+  const int nl = (in_cnt & 0xffff) + min(max(0, rem - (lo_cnt >> 16)), in_cnt >> 16);  // ... inside it
+  const int* lrows = rows + sel_lo;
   // attention over this rank's survivors: per-warp online softmax, log2 units
   float qf[4];
-  Raw4<T>::to_float(Raw4<T>::load(q + (int64_t)h * kHeadDim + lane * 4), qf);
+  Raw4<T>::to_float(q_raw, qf);
   const float scale = 0.088388347648318440f * kLog2e;
 #pragma unroll
   for (int j = 0; j < 4; ++j) qf[j] *= scale;
-  const T* Kh = K + (int64_t)hk * cap * kHeadDim + lane * 4;
-  const T* Vh = V + (int64_t)hk * cap * kHeadDim + lane * 4;
+  Kh += lane * 4;
+  Vh += lane * 4;
   float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
   for (int r = warp; r < nl; r += kSelThreads / 32) {
-    const int64_t t = rows[r];
+    const int64_t t = lrows[r] - rank_base;
     float kf[4], vf[4];
     Raw4<T>::to_float(Raw4<T>::load(Kh + t * kHeadDim), kf);
     Raw4<T>::to_float(Raw4<T>::load(Vh + t * kHeadDim), vf);
