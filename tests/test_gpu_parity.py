@@ -41,6 +41,40 @@ def test_encode_append_codes_bit_exact(gpu, oracle, bf16):
     assert cache.status() == 0
 
 
+@pytest.mark.parametrize("bf16", [False, True])
+def test_bulk_append_near_threshold_keys(gpu, oracle, bf16):
+    """Bulk prefill (the 8-lane encoder, four vectors per warp): keys built to
+    sit exactly on the 0 / +-kQ28 sigma thresholds after the transform, at
+    scales 1e-4 .. 1e4, mixed with random keys, ragged count; the uncertain
+    ones take the exact path, every code must equal the reference's."""
+    from oracle.bindings import bf16_round
+    rng = np.random.default_rng(23)
+    H = np.array([[1.0]])
+    for _ in range(7):
+        H = np.block([[H, H], [H, -H]])
+    H /= np.sqrt(128.0)
+    n_kv, S = 2, 517
+    K = rng.standard_normal((S, n_kv, 128))
+    for t in range(0, S, 3):
+        for h in range(n_kv):
+            y = rng.standard_normal(128)
+            sigma = np.sqrt(np.mean(y * y))
+            j = (t + h) % 128
+            y[j] = [0.0, 0.6744897501960817 * sigma, -0.6744897501960817 * sigma][(t // 3 + h) % 3]
+            K[t, h] = (H @ y) * 10.0 ** ((t % 9) - 4)
+    K = K.astype(np.float32)
+    if bf16:
+        K = bf16_round(K)
+    V = rng.standard_normal((S, n_kv, 128)).astype(np.float32)
+    if bf16:
+        V = bf16_round(V)
+    cache = fill_cache(gpu, K, V, bf16)
+    words = cache.code_words().cpu().numpy().view(np.uint16)
+    for h in range(n_kv):
+        assert np.array_equal(words[h], oracle.encode_pack_rows(K[:, h].astype(np.float64))), h
+    assert cache.status() == 0
+
+
 def test_query_encode_bit_exact_many(gpu, oracle):
     n = 4096
     _, _, q = make_inputs(1, 1, n, False, 12)
