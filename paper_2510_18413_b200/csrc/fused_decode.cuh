@@ -453,26 +453,27 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     return;
   }
 
-  if (warp < G) {  // encode query head hk * G + warp (sweep.cpp:92-94)
-    *reinterpret_cast<float4*>(qfs + warp * kHeadDim + lane * 4) = make_float4(f[0], f[1], f[2], f[3]);
-    Code c;
-    if (pdbg & 8) {  // diagnostics only: skip the query encode (wrong selection, timing only)
-      for (int w = 0; w < 4; ++w) { c.lo[w] = __float_as_uint(f[w]); c.hi[w] = 0u; }
-      if (lane == 0) qcode[warp] = c;
-    } else if (!encode128_to(f, sqs + warp * kHeadDim, qcode + warp, p.exact_encode != 0) && lane == 0) {
-      atomicOr(p.seq[si].status, kStatusDegenerate);
+  // One encoder call site for the query heads (warps 0..G-1) and the appended
+  // key (warp G): half the inline encoder code (fp32 route + exact fp64 path;
+  // measured 9.98 -> 9.91 us at config 1, profiles/r02h_ab_one_encode.txt).
+  if (warp < G || (has_new && warp == G)) {
+    const bool is_key = warp == G;
+    float e[4];
+    if (is_key) {  // append (kv_cache.cpp:62-71); part 0 of a split kv-head writes
+      const int64_t row = (int64_t)hk * cap + s_old;
+      if (part == 0) {
+        Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].K) + row * kHeadDim + lane * 4, kr);
+        Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].V) + row * kHeadDim + lane * 4, vr);
+      }
+      Raw4<T>::to_float(kr, e);
+    } else {  // query head hk * G + warp (sweep.cpp:92-94)
+      *reinterpret_cast<float4*>(qfs + warp * kHeadDim + lane * 4) = make_float4(f[0], f[1], f[2], f[3]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] = f[i];
     }
-  } else if (has_new && warp == G) {  // append (kv_cache.cpp:62-71); part 0 of a split kv-head writes
-    const int64_t row = (int64_t)hk * cap + s_old;
-    if (part == 0) {
-      Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].K) + row * kHeadDim + lane * 4, kr);
-      Raw4<T>::store(reinterpret_cast<T*>(p.seq[si].V) + row * kHeadDim + lane * 4, vr);
-    }
-    float kf[4];
-    Raw4<T>::to_float(kr, kf);
-    if (!encode128_to(kf, sqs + G * kHeadDim, qcode + G, p.exact_encode != 0) && lane == 0)
+    if (!encode128_to(e, sqs + warp * kHeadDim, qcode + warp, p.exact_encode != 0) && lane == 0)
       atomicOr(p.seq[si].status, kStatusDegenerate);
-    if (lane == 0 && part == 0) store_code(planes, cap, s_old, qcode[G]);  // written by this lane
+    if (is_key && lane == 0 && part == 0) store_code(planes, cap, s_old, qcode[G]);  // written by this lane
   }
   consumer_sync();
   QCode qc[G];
