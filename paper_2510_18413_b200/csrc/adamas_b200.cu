@@ -389,6 +389,10 @@ FusedPlan plan_for_split_c(int n_seqs, int n_kv, int n_q, int64_t s_max, int64_t
   if (C <= 0) {
     C = 1;
     while (C < 16 && units * C * 2 <= sm_count()) C *= 2;
+    // Prefer the one-hop exchange (C x G <= 8, the lean instance) while the
+    // rank stays short: measured 4 heads x 32K, C 16 (two hops) 8.20 us vs
+    // C 8 7.21 (profiles/r02z2_proxy_h4_c*.json).
+    while (C > 1 && C * G > 8 && (s_max + (int64_t)(C / 2) - 1) / (C / 2) <= 8192) C /= 2;
   }
   const int P = std::max(1, tu.P);
   for (;;) {

@@ -74,6 +74,11 @@ __device__ __forceinline__ float ld_mailbox(const float* p) {
   asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ float2 ld_mailbox2(const float* p) {
+  float2 v;
+  asm volatile("ld.relaxed.sys.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ float4 ld_mailbox4(const float* p) {
   float4 v;
   asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -380,14 +385,18 @@ __device__ __forceinline__ int encode128_warp_f32(const float in[4], Code& out) 
 // four butterfly stages are in-register, only three cross lanes (instead of
 // five at 4 elements per lane), and the network is left unnormalized:
 // Y = sqrt(128) y exactly in real arithmetic, and y > t  <=>  Y > kQ28 ||x||,
-// so no per-stage multiply is needed. Rounding bound (u = 2^-24): a stage-s
-// node holds a sum of 2^s inputs, |v| <= 2^(s/2) ||x||, and reaches an output
-// through 2^(7-s) ancestors, so |Y - Y_exact| <= u ||x|| sum_s 2^(7 - s/2)
-// = 282 u ||x|| = 1.7e-5 sigma in y units; the fp32 sum of squares and the
-// square root put the threshold within ~2.6e-6 sigma; the reference's fp64
-// values are within ~1e-14 sigma. A code is certain when Y is farther than
-// E = 2^-15 ||x|| (= 3.05e-5 sigma in y units, 1.6x the total) from every
-// threshold. Out (uniform within a group): res 1 certain / -1 not certified
+// so no per-stage multiply is needed. Rounding bound (u = 2^-24, first
+// order): the 2^(7-s) stage-s ancestors of an output are signed sums over a
+// partition of the inputs into sets of 2^s, so sum_j v_j^2 <= 2^s ||x||^2 and
+// (Cauchy-Schwarz) sum_j |v_j| <= sqrt(128) ||x||; each carries one rounding
+// <= u |v_j| into the output with weight +-1, so |Y - Y_exact| <=
+// 7 sqrt(128) u ||x||, i.e. 7 u ||x|| = 4.7e-6 sigma in y units (the
+// normalized 32-lane route's bound is 14 u ||x||: it also rounds a multiply
+// per stage). The fp32 sum of squares (19 additions of non-negative terms) and
+// the square root put the threshold within ~11 u t = 4.4e-7 sigma; the
+// reference's fp64 values are within ~1e-14 sigma. A code is certain when Y is
+// farther than E = 2^-15 ||x|| (= 3.05e-5 sigma in y units, ~6x the total)
+// from every threshold. Out (uniform within a group): res 1 certain / -1 not certified
 // (also for sums of squares outside [1e-30, 1e37]: the exact path decides,
 // including degenerate vectors); `out` = the group's code in every lane.
 __device__ __forceinline__ int encode128_g8_f32(const float (&in)[16], Code& out) {

@@ -595,6 +595,48 @@ constexpr int kSelMaxSurv = 2048;   // budget
 constexpr int kSelBins = 512;
 constexpr int kPartialStride = 132;  // m (natural-log units), l, pad, pad, o[128]
 
+// One warp: out[0..128) = sum_r e^{m_r - M} o_r / sum_r e^{m_r - M} l_r over
+// the n_ranks partials (m in natural-log units, l, pad, pad, o[128]) at
+// base + r * stride. Every load is independent of the others: lane r reads
+// rank r's (m, l) header, then every lane issues its o-quads of up to 8 ranks
+// at once — two round trips to the mailbox instead of one per rank and field.
+__device__ __forceinline__ void merge_partials_warp(const float* base, int64_t stride, int n_ranks, float* out_row) {
+  const int lane = threadIdx.x & 31;
+  float M = -INFINITY;
+  for (int r0 = 0; r0 < n_ranks; r0 += 32) {
+    const int r = r0 + lane;
+    const float2 ml = r < n_ranks ? ld_mailbox2(base + r * stride) : make_float2(-INFINITY, 0.f);
+    M = fmaxf(M, ml.y > 0.f ? ml.x : -INFINITY);
+  }
+#pragma unroll
+  for (int m2 = 16; m2 > 0; m2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, m2));
+  float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int r0 = 0; r0 < n_ranks; r0 += 32) {
+    const int r = r0 + lane;
+    const float2 ml = r < n_ranks ? ld_mailbox2(base + r * stride) : make_float2(-INFINITY, 0.f);
+    const float c = ml.y > 0.f ? __expf(ml.x - M) : 0.f;  // this lane's rank weight
+    L += warp_sum(ml.y * c);
+    const int nr = min(32, n_ranks - r0);
+    for (int q0 = 0; q0 < nr; q0 += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = q0 + i < nr ? ld_mailbox4(base + (r0 + q0 + i) * stride + 4 + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float ci = __shfl_sync(kFull, c, (q0 + i) & 31);
+        if (q0 + i < nr) {
+          acc[0] += v[i].x * ci; acc[1] += v[i].y * ci; acc[2] += v[i].z * ci; acc[3] += v[i].w * ci;
+        }
+      }
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  *reinterpret_cast<float4*>(out_row + lane * 4) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+}
+
+
+
 __device__ __forceinline__ void sel_block_excl_scan(int v, int& excl, int& total, int* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int incl = v;
@@ -811,26 +853,9 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   if (merge_out) {  // fused log-sum-exp merge of this q-head (every CTA of the launch is resident)
     if (tid == 0) peer_wait(merge_flags, n_ranks, push.epoch, status);
     __syncthreads();
-    if (warp == 0) {
-      float M = -INFINITY;
-      for (int r = 0; r < n_ranks; ++r) {
-        const float* pp = merge_parts + ((int64_t)r * n_q + h) * kPartialStride;
-        if (ld_mailbox(pp + 1) > 0.f) M = fmaxf(M, ld_mailbox(pp));
-      }
-      float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int r = 0; r < n_ranks; ++r) {
-        const float* pp = merge_parts + ((int64_t)r * n_q + h) * kPartialStride;
-        const float lr = ld_mailbox(pp + 1);
-        if (!(lr > 0.f)) continue;
-        const float c = __expf(ld_mailbox(pp) - M);
-        L += lr * c;
-        const float4 v = ld_mailbox4(pp + 4 + lane * 4);
-        acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
-      }
-      const float inv = L > 0.f ? 1.f / L : 0.f;
-      *reinterpret_cast<float4*>(merge_out + (int64_t)h * kHeadDim + lane * 4) =
-          make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    }
+    if (warp == 0)
+      merge_partials_warp(merge_parts + (int64_t)h * kPartialStride, (int64_t)n_q * kPartialStride, n_ranks,
+                          merge_out + (int64_t)h * kHeadDim);
   }
 }
 
@@ -845,24 +870,8 @@ __global__ void lse_merge_kernel(const float* partials, int n_ranks, int n_q, fl
     if (lane == 0) peer_wait(wait_flags, n_ranks, epoch, status);
     __syncwarp();
   }
-  float M = -INFINITY;
-  for (int r = 0; r < n_ranks; ++r) {
-    const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
-    if (ld_mailbox(pp + 1) > 0.f) M = fmaxf(M, ld_mailbox(pp));
-  }
-  float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int r = 0; r < n_ranks; ++r) {
-    const float* pp = partials + ((int64_t)r * n_q + h) * kPartialStride;
-    const float lr = ld_mailbox(pp + 1);
-    if (!(lr > 0.f)) continue;
-    const float c = __expf(ld_mailbox(pp) - M);
-    L += lr * c;
-    const float4 v = ld_mailbox4(pp + 4 + lane * 4);
-    acc[0] += v.x * c; acc[1] += v.y * c; acc[2] += v.z * c; acc[3] += v.w * c;
-  }
-  const float inv = L > 0.f ? 1.f / L : 0.f;
-  *reinterpret_cast<float4*>(out + (int64_t)h * kHeadDim + lane * 4) =
-      make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+  merge_partials_warp(partials + (int64_t)h * kPartialStride, (int64_t)n_q * kPartialStride, n_ranks,
+                      out + (int64_t)h * kHeadDim);
 }
 
 // An empty shard's candidates: all-empty keys into every mailbox, then the
