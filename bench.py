@@ -399,12 +399,14 @@ def run_ours(args):
                         keys_all[l].copy_(gather(keys))
                         part, _ = ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st)
                         parts_all[l].copy_(gather(part))
+                        ops.lse_merge(parts_all[l], stream=st, out=out[l, 0])
                     else:
+                        # the default N > 1 flow (peer memory) fuses select / attend / merge into one
+                        # launch; here the other shards' partials are in place, so the same fusion applies
                         ops.local_candidates(c, qs[s, l, 0], ks[s, l, 0], vs[s, l, 0], tail, base, B, stream=st,
                                              out=keys_all[l, my_slot])
-                        ops.select_attend(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, stream=st,
-                                          out=parts_all[l, my_slot])
-                    ops.lse_merge(parts_all[l], stream=st, out=out[l, 0])
+                        ops.select_attend_merge(c, qs[s, l, 0], keys_all[l], B, n_virtual * S, base, parts_all[l],
+                                                my_slot, stream=st, out=out[l, 0])
                     if tail:
                         c.truncate(S - 1)
     else:
@@ -566,7 +568,8 @@ def run_ours(args):
                              f"{L * NS * n_kv * S * (256 * es + 32) / 2**30:.1f} GiB > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "frac_of_8tbs": achieved / 8000.0,
-                         "kernel": ("fused candidates + seq_select_attend + lse_merge (3 launches per layer)"
+                         "kernel": ("fused candidates + seq_select_attend with the merge (2 launches per layer; "
+                                    "+ lse_merge with --exchange nccl at N > 1)"
                                     if seqshard else "fused_decode_kernel"), "bytes_per_launch": bytes_launch,
                          "kernel_us": kern_ms * 1000.0, "peak_source": peak_kind},
             "e2e": {"value": e2e_ms * 1000.0 / (n_e2e * L * tokens_per_layer), "unit": UNIT,

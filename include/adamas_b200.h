@@ -213,6 +213,16 @@ int adamas_seq_select_attend(const adamas_cache* cache, const void* q, int n_q_h
  * out float32 [n_q][128]. */
 int adamas_lse_merge(const float* partials, int n_ranks, int n_q_heads, float* out, void* stream);
 
+/* adamas_seq_select_attend + adamas_lse_merge in ONE launch, for callers whose
+ * other ranks' partials are already in `partials` [n_ranks][n_q][132] when it
+ * runs (this rank's goes to slot my_slot, then every q-head is merged into
+ * out [n_q][128]). The peer-memory step (adamas_seq_step_p2p) fuses the same
+ * way, waiting on the peers' epochs instead. Same sparse_attention /
+ * attention.cpp:8-45 semantics as the two calls. */
+int adamas_seq_select_attend_merge(const adamas_cache* cache, const void* q, int n_q_heads, const uint32_t* gathered,
+                                   int n_ranks, int64_t budget, int64_t total_len, int64_t rank_base, float* partials,
+                                   int my_slot, float* out, int32_t* global_idx, void* stream);
+
 /* ---------------------------------------------------------------- sequence sharding over peer memory
  * The same three phases as adamas_seq_local_candidates / _select_attend /
  * _lse_merge, with the two all-gathers replaced by stores into every rank's

@@ -29,7 +29,7 @@ EXPORTED = [
     "adamas_encode_query", "adamas_score", "adamas_topk", "adamas_sparse_attention",
     "adamas_decode_step", "adamas_decode_step_batched", "adamas_codes_ref_to_planes",
     "adamas_codes_planes_to_ref", "adamas_debug_trace", "adamas_seq_local_candidates",
-    "adamas_seq_select_attend", "adamas_lse_merge", "adamas_cache_save_adkv", "adamas_cache_load_adkv",
+    "adamas_seq_select_attend", "adamas_lse_merge", "adamas_seq_select_attend_merge", "adamas_cache_save_adkv", "adamas_cache_load_adkv",
     "adamas_score_metric", "adamas_hsel_create", "adamas_hsel_destroy", "adamas_hsel_build",
     "adamas_hsel_codes_ref", "adamas_hsel_select", "adamas_dot_topk", "adamas_page_select",
     "adamas_attention_f64", "adamas_topk_f64", "adamas_pages_create", "adamas_pages_destroy",
@@ -83,6 +83,7 @@ def load() -> C.CDLL:
     L.adamas_seq_local_candidates.argtypes = [vp, vp, i32, vp, vp, i32, i64, i64, vp, vp]
     L.adamas_seq_select_attend.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, vp, vp, vp]
     L.adamas_lse_merge.argtypes = [vp, i32, i32, vp, vp]
+    L.adamas_seq_select_attend_merge.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, vp, i32, vp, vp, vp]
     L.adamas_cache_save_adkv.argtypes = [vp, i32, C.c_char_p, vp]
     L.adamas_score_metric.argtypes = [vp, vp, i32, i32, vp, vp]
     L.adamas_cache_load_adkv.argtypes = [vp, C.POINTER(C.c_char_p), i32, vp]

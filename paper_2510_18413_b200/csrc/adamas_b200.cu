@@ -1050,31 +1050,57 @@ int adamas_seq_local_candidates(adamas_cache* c, const void* q, int n_q, const v
   return ADAMAS_OK;
 }
 
-int adamas_seq_select_attend(const adamas_cache* c, const void* q, int n_q, const uint32_t* gathered, int n_ranks,
-                             int64_t budget, int64_t total_len, int64_t rank_base, float* partial, int32_t* global_idx,
-                             void* stream) {
+namespace {
+// seq_select_attend_kernel launch for the gathered-keys path; with `out` the
+// same launch merges this rank's partial with the others' already in
+// `partials` (slot `my_slot` is this rank's).
+int launch_select_attend(const adamas_cache* c, const void* q, int n_q, const uint32_t* gathered, int n_ranks,
+                         int64_t budget, int64_t total_len, int64_t rank_base, float* partial, int32_t* global_idx,
+                         const float* merge_parts, float* out, cudaStream_t st) {
+  const int k_eff = (int)std::min<int64_t>(budget, total_len);
+  const int group = n_q / c->n_kv;
+  if (c->dtype == ADAMAS_BF16)
+    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<__nv_bfloat16>, dim3(n_q), dim3(kSelThreads),
+                           sel_smem(n_ranks, budget), st, (const __nv_bfloat16*)c->K, (const __nv_bfloat16*)c->V,
+                           c->capacity, group, (const __nv_bfloat16*)q, gathered, n_ranks, n_q, budget, k_eff,
+                           rank_base, c->seq_len, partial, global_idx, PeerPush{}, (const uint32_t*)nullptr, c->status,
+                           merge_parts, (const uint32_t*)nullptr, out));
+  else
+    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<float>, dim3(n_q), dim3(kSelThreads), sel_smem(n_ranks, budget),
+                           st, (const float*)c->K, (const float*)c->V, c->capacity, group, (const float*)q, gathered,
+                           n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{},
+                           (const uint32_t*)nullptr, c->status, merge_parts, (const uint32_t*)nullptr, out));
+  return launch_check("seq_select_attend_kernel");
+}
+
+int check_select_attend(const adamas_cache* c, const void* q, int n_q, const uint32_t* gathered, int n_ranks,
+                        int64_t budget, int64_t total_len, const float* partial) {
   if (int rc = check_cache(c)) return rc;
   if (int rc = check_heads(c, n_q)) return rc;
   if (n_ranks < 1 || budget < 1 || total_len < 1) return fail(ADAMAS_ERR_CONFIG, "seq_select_attend: bad sizes");
   if ((int64_t)n_ranks * budget > kSelMaxKeys || budget > kSelMaxSurv)
     return fail(ADAMAS_ERR_CONFIG, "seq_select_attend: n_ranks * budget exceeds 8192 (or budget > 2048)");
   if (!q || !gathered || !partial) return fail(ADAMAS_ERR_CONFIG, "seq_select_attend: null pointer");
-  const int k_eff = (int)std::min<int64_t>(budget, total_len);
-  const int group = n_q / c->n_kv;
-  if (c->dtype == ADAMAS_BF16)
-    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<__nv_bfloat16>, dim3(n_q), dim3(kSelThreads),
-                           sel_smem(n_ranks, budget), as_stream(stream), (const __nv_bfloat16*)c->K,
-                           (const __nv_bfloat16*)c->V, c->capacity, group, (const __nv_bfloat16*)q, gathered, n_ranks,
-                           n_q, budget, k_eff, rank_base, c->seq_len, partial, global_idx, PeerPush{},
-                           (const uint32_t*)nullptr, c->status, (const float*)nullptr, (const uint32_t*)nullptr,
-                           (float*)nullptr));
-  else
-    ADAMAS_CUDA(launch_pdl(seq_select_attend_kernel<float>, dim3(n_q), dim3(kSelThreads), sel_smem(n_ranks, budget),
-                           as_stream(stream), (const float*)c->K, (const float*)c->V, c->capacity, group,
-                           (const float*)q, gathered, n_ranks, n_q, budget, k_eff, rank_base, c->seq_len, partial,
-                           global_idx, PeerPush{}, (const uint32_t*)nullptr, c->status, (const float*)nullptr,
-                           (const uint32_t*)nullptr, (float*)nullptr));
-  return launch_check("seq_select_attend_kernel");
+  return ADAMAS_OK;
+}
+}  // namespace
+
+int adamas_seq_select_attend(const adamas_cache* c, const void* q, int n_q, const uint32_t* gathered, int n_ranks,
+                             int64_t budget, int64_t total_len, int64_t rank_base, float* partial, int32_t* global_idx,
+                             void* stream) {
+  if (int rc = check_select_attend(c, q, n_q, gathered, n_ranks, budget, total_len, partial)) return rc;
+  return launch_select_attend(c, q, n_q, gathered, n_ranks, budget, total_len, rank_base, partial, global_idx,
+                              nullptr, nullptr, as_stream(stream));
+}
+
+int adamas_seq_select_attend_merge(const adamas_cache* c, const void* q, int n_q, const uint32_t* gathered,
+                                   int n_ranks, int64_t budget, int64_t total_len, int64_t rank_base, float* partials,
+                                   int my_slot, float* out, int32_t* global_idx, void* stream) {
+  if (int rc = check_select_attend(c, q, n_q, gathered, n_ranks, budget, total_len, partials)) return rc;
+  if (my_slot < 0 || my_slot >= n_ranks || !out) return fail(ADAMAS_ERR_CONFIG, "seq_select_attend_merge: bad slot / out");
+  return launch_select_attend(c, q, n_q, gathered, n_ranks, budget, total_len, rank_base,
+                              partials + (int64_t)my_slot * n_q * kPartialStride, global_idx, partials, out,
+                              as_stream(stream));
 }
 
 int adamas_lse_merge(const float* partials, int n_ranks, int n_q, float* out, void* stream) {

@@ -9,10 +9,10 @@
 //   producer  one lane streams the rank's lo/x code planes through a ring of
 //             32 KB shared-memory stages with bulk copies (TMA engine), full /
 //             empty mbarriers per slot: no CTA-wide barrier in the scan
-//   prologue  consumer warps 0..G-1 encode the G query heads (fp64 FWHT + RMS
-//             thresholds, bit-exact) while the ring fills; the rank owning
-//             position S-1 encodes the new key and appends (k, v, code)
-//             (kv_cache.cpp:62-71)
+//   prologue  consumer warps 0..G-1 encode the G query heads (certified fp32
+//             FWHT + RMS thresholds, exact fp64 fallback: bit-exact) while the
+//             ring fills; in the rank owning position S-1, warp G encodes the
+//             new key and appends (k, v, code) (kv_cache.cpp:62-71)
 //   scan      each consumer thread turns two tokens per stage into G exact
 //             distances (estimator.cpp:45-59), stored as u16 in shared memory
 //             and counted in a per-CTA histogram per q-head

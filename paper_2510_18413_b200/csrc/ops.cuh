@@ -685,7 +685,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   // With the fused merge every CTA waits for every other CTA's partial, so all
   // must be resident: the next launch is not let in early (it could take the
   // SMs of CTAs not yet placed).
-  if (tid == 0 && merge_out == nullptr) grid_launch_dependents();
+  if (tid == 0 && (merge_out == nullptr || merge_flags == nullptr)) grid_launch_dependents();
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
   if (tid == 0) {
     s_T = -1; s_below = 0; s_bad = 0;
@@ -850,8 +850,9 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     __syncthreads();
     if (tid == 0) peer_signal(push);
   }
-  if (merge_out) {  // fused log-sum-exp merge of this q-head (every CTA of the launch is resident)
-    if (tid == 0) peer_wait(merge_flags, n_ranks, push.epoch, status);
+  if (merge_out) {  // fused log-sum-exp merge of this q-head (with merge_flags: every CTA of the launch is
+                   // resident; without: the other ranks' partials are already in place)
+    if (tid == 0 && merge_flags) peer_wait(merge_flags, n_ranks, push.epoch, status);
     __syncthreads();
     if (warp == 0)
       merge_partials_warp(merge_parts + (int64_t)h * kPartialStride, (int64_t)n_q * kPartialStride, n_ranks,

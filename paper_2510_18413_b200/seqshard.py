@@ -72,6 +72,19 @@ class CudaSeqOps:
                                               total_len, base, _ptr(partial), _ptr(gidx), _stream(stream)))
         return partial, gidx
 
+    def select_attend_merge(self, cache, q, gathered, budget: int, total_len: int, base: int, partials,
+                            my_slot: int, want_idx=False, stream=None, out=None):
+        """select_attend + lse_merge in one launch, for partials of the other
+        ranks already in place (this rank's goes to partials[my_slot])."""
+        n_q = q.numel() // HEAD_DIM
+        world = gathered.shape[0]
+        out = out if out is not None else torch.empty((n_q, HEAD_DIM), dtype=torch.float32, device=q.device)
+        gidx = torch.empty((n_q, budget), dtype=torch.int32, device=q.device) if want_idx else None
+        check(self.L.adamas_seq_select_attend_merge(cache.h, _ptr(q), n_q, _ptr(gathered.contiguous()), world, budget,
+                                                    total_len, base, _ptr(partials), my_slot, _ptr(out), _ptr(gidx),
+                                                    _stream(stream)))
+        return out, gidx
+
     def lse_merge(self, partials, stream=None, out=None):
         world, n_q = partials.shape[0], partials.shape[1]
         out = out if out is not None else torch.empty((n_q, HEAD_DIM), dtype=torch.float32, device=partials.device)

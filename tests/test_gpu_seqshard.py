@@ -149,3 +149,38 @@ def test_mailbox_errors(gpu):
     with pytest.raises(ConfigError, match="not connected"):
         dec.local_p2p(box, q, None, None)
     assert len(box.ipc_handle()) == Mailbox.HANDLE_BYTES
+
+
+@pytest.mark.parametrize("W,n_kv,G,budget,bf16", [(8, 2, 4, 128, True), (3, 1, 2, 64, False)])
+def test_select_attend_merge_equals_two_launches(gpu, oracle, W, n_kv, G, budget, bf16):
+    """adamas_seq_select_attend_merge (one launch: this rank's partial into its
+    slot, then the log-sum-exp merge over every slot) against
+    adamas_seq_select_attend + adamas_lse_merge: identical outputs and indices,
+    and the oracle's selection over the whole sequence."""
+    from paper_2510_18413_b200.seqshard import CudaSeqOps
+    ops = CudaSeqOps()
+    S = 600 * W
+    n_q = n_kv * G
+    K, V, q = make_inputs(S, n_kv, n_q, bf16, 31 + W)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    per = S // W
+    caches = []
+    for r in range(W):
+        c = gpu.KvCache(n_kv, per + 4, dt)
+        c.update(to_dev(K[r * per:(r + 1) * per], bf16), to_dev(V[r * per:(r + 1) * per], bf16))
+        caches.append(c)
+    qd = to_dev(q, bf16)
+    keys = torch.stack([ops.local_candidates(caches[r], qd, None, None, False, r * per, budget) for r in range(W)])
+    parts = torch.stack([ops.select_attend(caches[r], qd, keys, budget, S, r * per)[0] for r in range(W)])
+    ref_out = ops.lse_merge(parts)
+    _, ref_idx = ops.select_attend(caches[0], qd, keys, budget, S, 0, want_idx=True)
+    _, _, eidx, _ = oracle_decode(oracle, K, V, q, budget)
+    assert np.array_equal(ref_idx.cpu().numpy(), eidx)
+    for r in range(W):
+        buf = parts.clone()
+        buf[r].fill_(float("nan"))  # this rank's slot is written by the launch itself
+        out, gidx = ops.select_attend_merge(caches[r], qd, keys, budget, S, r * per, buf, r, want_idx=True)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_out), r
+        assert torch.equal(buf[r], parts[r]), r
+        assert np.array_equal(gidx.cpu().numpy(), eidx), r
