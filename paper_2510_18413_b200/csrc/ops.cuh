@@ -589,6 +589,9 @@ namespace adamas_dev {
 // exactly the single-device one. One CTA per q-head rebuilds it, attends over
 // this rank's survivors (rows of the local cache) and emits the partial
 // (m, l, o[128]) for the log-sum-exp merge (attention.cpp:8-38 semantics).
+#ifndef ADAMAS_SEL_STOP
+#define ADAMAS_SEL_STOP 0  // diagnostics builds only: stop seq_select_attend after phase N (timing only)
+#endif
 constexpr int kSelThreads = 512;
 constexpr int kSelMaxKeys = 8192;   // n_ranks * budget per q-head
 constexpr int kSelMaxSurv = 2048;   // budget
@@ -647,14 +650,17 @@ __device__ __forceinline__ void sel_block_excl_scan(int v, int& excl, int& total
   }
   if (lane == 31) scratch[warp] = incl;
   __syncthreads();
-  int before = 0, sum = 0;
-  for (int w = 0; w < kSelThreads / 32; ++w) {
-    const int x = scratch[w];
-    before += w < warp ? x : 0;
-    sum += x;
+  // the 16 warp totals: a 4-step shuffle scan (not a serial walk) in every warp
+  constexpr int NW = kSelThreads / 32;
+  int wt = lane < NW ? scratch[lane] : 0;
+#pragma unroll
+  for (int m = 1; m < NW; m <<= 1) {
+    const int o = __shfl_up_sync(kFull, wt, m);
+    if (lane >= m) wt += o;
   }
-  excl = before + incl - v;
-  total = sum;
+  const int before = __shfl_sync(kFull, wt, (warp + 31) & 31);  // inclusive total of warps < warp
+  excl = (warp > 0 ? before : 0) + incl - v;
+  total = __shfl_sync(kFull, wt, NW - 1);
   __syncthreads();
 }
 
@@ -675,7 +681,13 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   __shared__ int rows[kSelMaxSurv];  // this rank's survivors (local rows), ascending
   __shared__ float wm[kSelThreads / 32], wl[kSelThreads / 32];
   __shared__ float wo[kSelThreads / 32][kHeadDim];
+  __shared__ __align__(16) float pre_s[8][kPartialStride];  // fused merge, partials in place: every rank's
   const int h = blockIdx.x, hk = h / group;
+  // Fused merge whose other partials are already in place (no peer epochs to
+  // wait for): they are read at the start, behind the selection, and merged
+  // from shared memory with this rank's partial at the end.
+  const bool merge_local = merge_out != nullptr && merge_flags == nullptr && partial != nullptr && n_ranks <= 8;
+  const int my_slot = merge_local ? (int)((partial - merge_parts) / ((int64_t)n_q * kPartialStride)) : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = n_ranks * (int)budget;
   constexpr uint32_t kEmpty = 0xffffffffu;
@@ -686,6 +698,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   // must be resident: the next launch is not let in early (it could take the
   // SMs of CTAs not yet placed).
   if (tid == 0 && (merge_out == nullptr || merge_flags == nullptr)) grid_launch_dependents();
+  if (ADAMAS_SEL_STOP == 9) return;  // diagnostics (timing only)
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
   if (tid == 0) {
     s_T = -1; s_below = 0; s_bad = 0;
@@ -697,6 +710,11 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   const T* Kh = K + (int64_t)hk * cap * kHeadDim;
   const T* Vh = V + (int64_t)hk * cap * kHeadDim;
   __syncthreads();
+  constexpr int kQuads = kPartialStride / 4;
+  const int pr_r = tid / kQuads, pr_c = tid - pr_r * kQuads;
+  const bool pre_mine = merge_local && pr_r < n_ranks && pr_r != my_slot;
+  float4 pre_v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (pre_mine) pre_v = ld_mailbox4(merge_parts + ((int64_t)pr_r * n_q + h) * kPartialStride + pr_c * 4);
   {
     int r = tid / (int)budget, i = tid - r * (int)budget;  // j = r * budget + i, advanced without a division
     for (int j = tid; j < n; j += kSelThreads) {
@@ -718,7 +736,9 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
       for (i += kSelThreads; i >= (int)budget; i -= (int)budget) ++r;
     }
   }
+  if (pre_mine) *reinterpret_cast<float4*>(&pre_s[pr_r][pr_c * 4]) = pre_v;
   __syncthreads();
+  if (ADAMAS_SEL_STOP == 1) return;  // diagnostics (timing only)
   // Input contract (adamas_seq_local_candidates): each rank's keys ascending
   // in the index field, empty keys last; ranks in sequence order. The array
   // is then ascending in index, so an order-preserving compaction emits the
@@ -745,6 +765,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     if (tid == 0) atomicOr(status, kStatusBadSelection);
     return;  // (the peer-exchange launch's waiters time out on the missing partial and latch it too)
   }
+  if (ADAMAS_SEL_STOP == 2) return;  // diagnostics (timing only)
   // Keys are unique (dist << 23 | global index) and the array ascends in the
   // index field, so the selection -- the k_eff smallest keys in top_k's
   // (score, index) order -- is every key at distance < T plus the first
@@ -799,6 +820,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   const int sel_lo = (lo_cnt & 0xffff) + min(rem, lo_cnt >> 16);  // selected below the local range
   const int nl = (in_cnt & 0xffff) + min(max(0, rem - (lo_cnt >> 16)), in_cnt >> 16);  // ... inside it
   const int* lrows = rows + sel_lo;
+  if (ADAMAS_SEL_STOP == 3) return;  // diagnostics (timing only)
   // attention over this rank's survivors: per-warp online softmax, log2 units
   float qf[4];
   Raw4<T>::to_float(q_raw, qf);
@@ -808,18 +830,52 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   Kh += lane * 4;
   Vh += lane * 4;
   float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int r = warp; r < nl; r += kSelThreads / 32) {
-    const int64_t t = lrows[r] - rank_base;
-    float kf[4], vf[4];
-    Raw4<T>::to_float(Raw4<T>::load(Kh + t * kHeadDim), kf);
-    Raw4<T>::to_float(Raw4<T>::load(Vh + t * kHeadDim), vf);
-    const float sd = warp_sum(qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3]);
-    const float mn = fmaxf(m, sd);
-    const float corr = exp2f(m - mn), pr = exp2f(sd - mn);
-    l = l * corr + pr;
+  constexpr int NW = kSelThreads / 32, B = 4;  // rows in flight per warp (all survivors may be local)
+  for (int r0 = warp; r0 < nl; r0 += NW * B) {
+    typename Raw4<T>::V kb[B], vb[B];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = o[j] * corr + pr * vf[j];
-    m = mn;
+    for (int b = 0; b < B; ++b) {
+      const int r = r0 + b * NW;
+      if (r < nl) {
+        const int64_t t = lrows[r] - rank_base;
+        kb[b] = Raw4<T>::load(Kh + t * kHeadDim);
+        vb[b] = Raw4<T>::load(Vh + t * kHeadDim);
+      } else {
+        kb[b] = typename Raw4<T>::V{};
+        vb[b] = typename Raw4<T>::V{};
+      }
+    }
+    float sd[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float kf[4];
+      Raw4<T>::to_float(kb[b], kf);
+      sd[b] = r0 + b * NW < nl ? qf[0] * kf[0] + qf[1] * kf[1] + qf[2] * kf[2] + qf[3] * kf[3] : 0.f;
+    }
+#pragma unroll
+    for (int m2 = 16; m2 > 0; m2 >>= 1)
+#pragma unroll
+      for (int b = 0; b < B; ++b) sd[b] += __shfl_xor_sync(kFull, sd[b], m2);
+    float mx = m;
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (r0 + b * NW < nl) mx = fmaxf(mx, sd[b]);
+    const float corr = exp2f(m - mx);
+    l *= corr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] *= corr;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (r0 + b * NW < nl) {
+        float vf[4];
+        Raw4<T>::to_float(vb[b], vf);
+        const float pr = exp2f(sd[b] - mx);
+        l += pr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] += pr * vf[j];
+      }
+    }
+    m = mx;
   }
   if (lane == 0) { wm[warp] = m; wl[warp] = l; }
 #pragma unroll
@@ -845,13 +901,34 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
       if (lane == 0) *reinterpret_cast<float4*>(pp) = hdr;
       *reinterpret_cast<float4*>(pp + 4 + lane * 4) = body;
     }
+    if (merge_local) {  // this rank's partial joins the preloaded ones; merge from shared memory
+      if (lane == 0) *reinterpret_cast<float4*>(&pre_s[my_slot][0]) = hdr;
+      *reinterpret_cast<float4*>(&pre_s[my_slot][4 + lane * 4]) = body;
+      __syncwarp();
+      const float2 ml = lane < n_ranks ? make_float2(pre_s[lane][0], pre_s[lane][1]) : make_float2(-INFINITY, 0.f);
+      float Mx = ml.y > 0.f ? ml.x : -INFINITY;
+#pragma unroll
+      for (int m2 = 16; m2 > 0; m2 >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(kFull, Mx, m2));
+      const float cr = ml.y > 0.f ? __expf(ml.x - Mx) : 0.f;
+      const float Ls = warp_sum(ml.y * cr);
+      float a2[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int r = 0; r < n_ranks; ++r) {
+        const float c = __shfl_sync(kFull, cr, r);
+        const float4 v = *reinterpret_cast<const float4*>(&pre_s[r][4 + lane * 4]);
+        a2[0] += v.x * c; a2[1] += v.y * c; a2[2] += v.z * c; a2[3] += v.w * c;
+      }
+      const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
+      *reinterpret_cast<float4*>(merge_out + (int64_t)h * kHeadDim + lane * 4) =
+          make_float4(a2[0] * inv, a2[1] * inv, a2[2] * inv, a2[3] * inv);
+    }
   }
   if (push.n) {
     __syncthreads();
     if (tid == 0) peer_signal(push);
   }
-  if (merge_out) {  // fused log-sum-exp merge of this q-head (with merge_flags: every CTA of the launch is
-                   // resident; without: the other ranks' partials are already in place)
+  if (ADAMAS_SEL_STOP == 4) return;  // diagnostics (timing only)
+  if (merge_out && !merge_local) {  // fused log-sum-exp merge of this q-head (with merge_flags: every CTA
+                                   // of the launch is resident; without: the other ranks' partials are in place)
     if (tid == 0 && merge_flags) peer_wait(merge_flags, n_ranks, push.epoch, status);
     __syncthreads();
     if (warp == 0)
