@@ -589,6 +589,9 @@ namespace adamas_dev {
 // exactly the single-device one. One CTA per q-head rebuilds it, attends over
 // this rank's survivors (rows of the local cache) and emits the partial
 // (m, l, o[128]) for the log-sum-exp merge (attention.cpp:8-38 semantics).
+#ifndef ADAMAS_SEL_MINB
+#define ADAMAS_SEL_MINB 1
+#endif
 #ifndef ADAMAS_SEL_STOP
 #define ADAMAS_SEL_STOP 0  // diagnostics builds only: stop seq_select_attend after phase N (timing only)
 #endif
@@ -665,7 +668,7 @@ __device__ __forceinline__ void sel_block_excl_scan(int v, int& excl, int& total
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSelThreads)
+__global__ void __launch_bounds__(kSelThreads, ADAMAS_SEL_MINB)
 seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
                          const T* __restrict__ q, const uint32_t* keys, int n_ranks, int n_q,
                          int64_t budget, int k_eff, int64_t rank_base, int64_t rank_len, float* __restrict__ partial,
@@ -680,7 +683,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   __shared__ int s_lo_cnt, s_in_cnt;  // packed (lt | eq << 16) counts below / inside the local range
   __shared__ int rows[kSelMaxSurv];  // this rank's survivors (local rows), ascending
   __shared__ float wm[kSelThreads / 32], wl[kSelThreads / 32];
-  __shared__ float wo[kSelThreads / 32][kHeadDim];
+  __shared__ __align__(16) float wo[kSelThreads / 32][kHeadDim];
   __shared__ __align__(16) float pre_s[8][kPartialStride];  // fused merge, partials in place: every rank's
   const int h = blockIdx.x, hk = h / group;
   // Fused merge whose other partials are already in place (no peer epochs to
@@ -836,7 +839,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int r = r0 + b * NW;
-      if (r < nl) {
+      if (r < nl && ADAMAS_SEL_STOP != 5) {
         const int64_t t = lrows[r] - rank_base;
         kb[b] = Raw4<T>::load(Kh + t * kHeadDim);
         vb[b] = Raw4<T>::load(Vh + t * kHeadDim);
@@ -877,21 +880,27 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
     }
     m = mx;
   }
+  if (ADAMAS_SEL_STOP == 6) {  // diagnostics (timing only): attention done, no combine
+    if (lane == 0 && m == 12345.f) partial[0] = l;
+    return;
+  }
   if (lane == 0) { wm[warp] = m; wl[warp] = l; }
 #pragma unroll
   for (int j = 0; j < 4; ++j) wo[warp][lane * 4 + j] = o[j];
   __syncthreads();
-  if (warp == 0) {
-    float M = -INFINITY;
-    for (int w = 0; w < kSelThreads / 32; ++w)
-      if (wl[w] > 0.f) M = fmaxf(M, wm[w]);
-    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int w = 0; w < kSelThreads / 32; ++w) {
-      if (!(wl[w] > 0.f)) continue;
-      const float c = exp2f(wm[w] - M);
-      L += wl[w] * c;
+  if (warp == 0) {  // combine the NW warp partials: lane-parallel weights, all quads in flight
+    const float mw = lane < NW ? wm[lane] : -INFINITY, lw = lane < NW ? wl[lane] : 0.f;
+    float M = lw > 0.f ? mw : -INFINITY;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] += wo[w][lane * 4 + j] * c;
+    for (int m2 = 16; m2 > 0; m2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, m2));
+    const float cw = lw > 0.f ? exp2f(mw - M) : 0.f;
+    const float L = warp_sum(lw * cw);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float c = __shfl_sync(kFull, cw, w);
+      const float4 v4 = *reinterpret_cast<const float4*>(&wo[w][lane * 4]);
+      acc[0] += v4.x * c; acc[1] += v4.y * c; acc[2] += v4.z * c; acc[3] += v4.w * c;
     }
     const float4 hdr = make_float4(L > 0.f ? M / kLog2e : -INFINITY, L, 0.f, 0.f);  // natural-log units
     const float4 body = make_float4(acc[0], acc[1], acc[2], acc[3]);
