@@ -284,14 +284,16 @@ __device__ __forceinline__ bool encode128_to(const float in[4], double* sq, Code
 // registers, so only where needed), 0 = 32-token groups per thread for ranks
 // longer than that. Each instance carries one form only (measured: 1.6 %
 // faster than choosing at run time).
-// FULL: the two-hop histogram exchange (C x G > 8), multi-cluster units
+// MODE 1 (FULL): the two-hop histogram exchange (C x G > 8), multi-cluster units
 // (P > 1) and candidates mode are compiled in; the common one-hop decode
 // launches an instance without them (measured 3.6-4.8 % faster at configs
 // 1-3: fewer registers, 71 KB instead of 125 KB of code).
 // CT: the cluster size when fixed at compile time (the common C = 4 decode
 // launch; measured 3 % faster), 0 = from the launch parameters.
-template <typename T, int G, int SW, bool FULL, int CT>
+template <typename T, int G, int SW, int MODE, int CT>
 __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel(const __grid_constant__ FusedParams p) {
+  constexpr bool FULL = MODE == 1;  // two-hop exchange, multi-cluster units and candidates mode compiled in
+  constexpr bool CAND = MODE != 0;  // candidates mode compiled in (MODE 2: with the lean one-hop exchange only)
   static_assert(G >= 1 && G <= kMaxG && (kConsumerWarps % G) == 0, "G must divide the warp count");
   constexpr int WG = kConsumerWarps / G;  // consumer warps per q-head
   constexpr int NT = kConsumers / G;      // consumer threads per q-head
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
   // diagnostics (phase stamps, timing-only switches) exist only in ADAMAS_DIAG builds
   const int pdbg = ADAMAS_DIAG ? p.dbg : 0;
   unsigned long long* const ptrace = ADAMAS_DIAG ? p.trace : nullptr;
-  uint32_t* const pcand = FULL ? p.cand : nullptr;  // candidates mode (sequence sharding)
+  uint32_t* const pcand = CAND ? p.cand : nullptr;  // candidates mode (sequence sharding)
   const int pc = (blockIdx.x / C) % P;  // this cluster's token range within the unit
   const int gr = pc * C + rank;          // rank over the unit's P * C CTAs
   const int unit = blockIdx.x / (C * P);
