@@ -454,7 +454,9 @@ def run_ours(args):
         ad.set_tuning(**saved_tuning)
         isolated = {"value": iso_ms * 1000.0 / (n_iso * L * NS), "unit": UNIT,
                     "note": "same steps with programmatic dependent launch off: no layer overlaps its predecessor"}
-    launches_per_step = L * (3 if seqshard else 1)
+    # seqshard: candidates + select / attend / merge (N = 1 proxy and the p2p step when every select CTA
+    # is co-resident: 2 launches per layer); the NCCL flow adds lse_merge (3)
+    launches_per_step = L * ((3 if ws > 1 and args.exchange == "nccl" else 2) if seqshard else 1)
     ms_per_step = elapsed_ms / args.steps
     tokens_per_layer = NS  # one decoded token per sequence per layer
     us_per_token_layer = ms_per_step * 1000.0 / (L * tokens_per_layer)
