@@ -151,8 +151,15 @@ __device__ __forceinline__ void csa3(uint32_t a, uint32_t b, uint32_t c, uint32_
 // ah ^ bh = X ^ kx ^ L with X = al ^ ah, kx = bl ^ bh, so A is ONE 3-input
 // LOP3 of (X, kx, L). Checked exhaustively over all 16 (a, b) pairs in
 // tests/test_abi.py. The 4 weight-1 words L and 4 weight-2 words A are folded
-// by carry-save adders into 5 popcounts (balances the ALU and XU pipes; see
-// tools/scan_bench.cu).
+// by carry-save adders into fewer popcounts (trading ALU LOP3s against the
+// quarter-rate POPC pipe; see below and tools/scan_bench.cu).
+// Three carry-save foldings of the same sum, picked per kernel instance by
+// measurement (tools/ab.sh, profiles/r02h_ab_distance_fold.txt): FOLD 6 —
+// 6 POPC, 12 LOP3 (the default: best at one q-head per scan, config 1 9.93 ->
+// 9.89 us, config 2 16.80 -> 16.41); FOLD 7 — 7 POPC, 10 LOP3 (best for
+// ALU-bound multi-head scans, config 3 4.20 -> 4.07); FOLD 5 — 5 POPC, 16
+// LOP3 (the round-1 balance). All return the identical integer.
+template <int FOLD = 6>
 __device__ __forceinline__ uint32_t l1_distance(const QCode& q, const uint32_t klo[4], const uint32_t kx[4]) {
   uint32_t L[4], A[4];
 #pragma unroll
@@ -160,12 +167,23 @@ __device__ __forceinline__ uint32_t l1_distance(const QCode& q, const uint32_t k
     L[w] = q.lo[w] ^ klo[w];
     A[w] = (q.x[w] ^ kx[w] ^ L[w]) & ~(L[w] & q.x[w]);
   }
-  uint32_t s1, c1, s2, c2, s3, c3;
-  csa3(L[0], L[1], L[2], s1, c1);                    // weight 1: s1, weight 2: c1
-  const uint32_t s1b = s1 ^ L[3], c1b = s1 & L[3];   // weight 1: s1b, weight 2: c1b
-  csa3(A[0], A[1], A[2], s2, c2);                    // weight 2: s2, weight 4: c2
-  csa3(A[3], c1, c1b, s3, c3);                       // weight 2: s3, weight 4: c3
-  return __popc(s1b) + 2u * (__popc(s2) + __popc(s3)) + 4u * (__popc(c2) + __popc(c3));
+  if constexpr (FOLD == 7) {
+    uint32_t s1, c1;
+    csa3(L[0], L[1], L[2], s1, c1);  // weight 1: s1, weight 2: c1
+    return __popc(s1) + __popc(L[3]) + 2u * (__popc(c1) + __popc(A[0]) + __popc(A[1]) + __popc(A[2]) + __popc(A[3]));
+  } else if constexpr (FOLD == 6) {
+    uint32_t s1, c1, s2, c2;
+    csa3(L[0], L[1], L[2], s1, c1);  // weight 1: s1, weight 2: c1
+    csa3(A[0], A[1], A[2], s2, c2);  // weight 2: s2, weight 4: c2
+    return __popc(s1) + __popc(L[3]) + 2u * (__popc(c1) + __popc(s2) + __popc(A[3])) + 4u * __popc(c2);
+  } else {
+    uint32_t s1, c1, s2, c2, s3, c3;
+    csa3(L[0], L[1], L[2], s1, c1);                    // weight 1: s1, weight 2: c1
+    const uint32_t s1b = s1 ^ L[3], c1b = s1 & L[3];   // weight 1: s1b, weight 2: c1b
+    csa3(A[0], A[1], A[2], s2, c2);                    // weight 2: s2, weight 4: c2
+    csa3(A[3], c1, c1b, s3, c3);                       // weight 2: s3, weight 4: c3
+    return __popc(s1b) + 2u * (__popc(s2) + __popc(s3)) + 4u * (__popc(c2) + __popc(c3));
+  }
 }
 
 // Streaming 128-bit load (no L1 allocation).

@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kFusedThreads, kCtasPerSm) fused_decode_kernel
     for (int u = 0; u < kTokPerThread; ++u) {
       const uint32_t lo[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, x[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
 #pragma unroll
-      for (int g = 0; g < G; ++g) d[u][g] = l1_distance(qc[g], lo, x);
+      for (int g = 0; g < G; ++g) d[u][g] = l1_distance<G >= 2 ? 7 : 6>(qc[g], lo, x);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[slot]);  // this warp is done reading the slot

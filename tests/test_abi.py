@@ -79,7 +79,7 @@ def test_bitplane_distance_identity_exhaustive():
 
 
 def test_carry_save_popcount_fold():
-    """The 5-popcount carry-save fold in l1_distance equals sum popc(L) + 2 sum popc(A)."""
+    """Every carry-save fold in l1_distance (5, 6 or 7 popcounts) equals sum popc(L) + 2 sum popc(A)."""
     rng = np.random.default_rng(3)
     popc = lambda x: bin(int(x)).count("1")  # noqa: E731
     for _ in range(3000):
@@ -91,7 +91,12 @@ def test_carry_save_popcount_fold():
         s2, c2 = csa(A[0], A[1], A[2])
         s3, c3 = csa(A[3], c1, c1b)
         got = popc(s1b) + 2 * (popc(s2) + popc(s3)) + 4 * (popc(c2) + popc(c3))
-        assert got == sum(map(popc, L)) + 2 * sum(map(popc, A))
+        want = sum(map(popc, L)) + 2 * sum(map(popc, A))
+        assert got == want
+        # FOLD 6 (6 popcounts) and FOLD 7 (7 popcounts), the instances' choices
+        f6 = popc(s1) + popc(L[3]) + 2 * (popc(c1) + popc(s2) + popc(A[3])) + 4 * popc(c2)
+        f7 = popc(s1) + popc(L[3]) + 2 * (popc(c1) + sum(map(popc, A)))
+        assert f6 == want and f7 == want
 
 
 def test_bitplane_distance_matches_oracle_on_words(oracle):
