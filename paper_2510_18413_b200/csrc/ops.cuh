@@ -589,9 +589,6 @@ namespace adamas_dev {
 // exactly the single-device one. One CTA per q-head rebuilds it, attends over
 // this rank's survivors (rows of the local cache) and emits the partial
 // (m, l, o[128]) for the log-sum-exp merge (attention.cpp:8-38 semantics).
-#ifndef ADAMAS_SEL_MINB
-#define ADAMAS_SEL_MINB 1
-#endif
 #ifndef ADAMAS_SEL_STOP
 #define ADAMAS_SEL_STOP 0  // diagnostics builds only: stop seq_select_attend after phase N (timing only)
 #endif
@@ -668,7 +665,7 @@ __device__ __forceinline__ void sel_block_excl_scan(int v, int& excl, int& total
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSelThreads, ADAMAS_SEL_MINB)
+__global__ void __launch_bounds__(kSelThreads)
 seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64_t cap, int group,
                          const T* __restrict__ q, const uint32_t* keys, int n_ranks, int n_q,
                          int64_t budget, int k_eff, int64_t rank_base, int64_t rank_len, float* __restrict__ partial,
