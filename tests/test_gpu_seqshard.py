@@ -151,7 +151,7 @@ def test_mailbox_errors(gpu):
     assert len(box.ipc_handle()) == Mailbox.HANDLE_BYTES
 
 
-@pytest.mark.parametrize("W,n_kv,G,budget,bf16", [(8, 2, 4, 128, True), (3, 1, 2, 64, False)])
+@pytest.mark.parametrize("W,n_kv,G,budget,bf16", [(8, 2, 4, 128, True), (3, 1, 2, 64, False), (12, 1, 4, 64, True)])
 def test_select_attend_merge_equals_two_launches(gpu, oracle, W, n_kv, G, budget, bf16):
     """adamas_seq_select_attend_merge (one launch: this rank's partial into its
     slot, then the log-sum-exp merge over every slot) against
