@@ -126,7 +126,7 @@ struct __align__(32) Code {
 
 // Query-side precomputation for the distance: X = lo ^ hi.
 struct QCode {
-  uint32_t lo[4], x[4];
+  uint32_t lo[4], x[4], hi[4];
 };
 
 __device__ __forceinline__ QCode make_qcode(const Code& c) {
@@ -135,8 +135,18 @@ __device__ __forceinline__ QCode make_qcode(const Code& c) {
   for (int w = 0; w < 4; ++w) {
     q.lo[w] = c.lo[w];
     q.x[w] = c.lo[w] ^ c.hi[w];
+    q.hi[w] = c.hi[w];
   }
   return q;
+}
+
+// One LOP3 with an explicit truth table (the compiler's own fusion of the
+// A term below took 5 instructions per word instead of 3).
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
 }
 
 // Carry-save adder: a + b + c = s + 2 cy, bitwise.
@@ -165,7 +175,16 @@ __device__ __forceinline__ uint32_t l1_distance(const QCode& q, const uint32_t k
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     L[w] = q.lo[w] ^ klo[w];
-    A[w] = (q.x[w] ^ kx[w] ^ L[w]) & ~(L[w] & q.x[w]);
+    if constexpr (FOLD == 7) {
+      // ah ^ bh = qh ^ kl ^ kx: one 3-input XOR independent of L; then
+      // A = H & ~(L & X) is one more LOP3 (truth table 0xF0 & ~(0xCC & 0xAA)).
+      // Measured: multi-head scans 4.07 -> 3.97 us (config 3); at one q-head
+      // per scan the compiler's own form is faster (kept for FOLD 6).
+      const uint32_t H = lop3<0x96>(q.hi[w], klo[w], kx[w]);
+      A[w] = lop3<0x70>(H, L[w], q.x[w]);
+    } else {
+      A[w] = (q.x[w] ^ kx[w] ^ L[w]) & ~(L[w] & q.x[w]);
+    }
   }
   if constexpr (FOLD == 7) {
     uint32_t s1, c1;
