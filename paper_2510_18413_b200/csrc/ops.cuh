@@ -681,7 +681,7 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   __shared__ int rows[kSelMaxSurv];  // this rank's survivors (local rows), ascending
   __shared__ float wm[kSelThreads / 32], wl[kSelThreads / 32];
   __shared__ __align__(16) float wo[kSelThreads / 32][kHeadDim];
-  __shared__ __align__(16) float pre_s[8][kPartialStride];  // fused merge, partials in place: every rank's
+  __shared__ __align__(16) float pre_s[8][kPartialStride];  // local fused merge: every rank's partial
   const int h = blockIdx.x, hk = h / group;
   // Fused merge whose other partials are already in place (no peer epochs to
   // wait for): they are read at the start, behind the selection, and merged
@@ -694,9 +694,9 @@ seq_select_attend_kernel(const T* __restrict__ K, const T* __restrict__ V, int64
   // programmatic dependent launch: keys / the appended row come from the
   // preceding kernel; the next launch may begin its own prologue now
   grid_dependency_wait();
-  // With the fused merge every CTA waits for every other CTA's partial, so all
-  // must be resident: the next launch is not let in early (it could take the
-  // SMs of CTAs not yet placed).
+  // With the peer-epoch merge (merge_flags) every CTA waits for the other
+  // ranks' partials, so all must be resident: the next launch is not let in
+  // early (it could take the SMs of CTAs not yet placed).
   if (tid == 0 && (merge_out == nullptr || merge_flags == nullptr)) grid_launch_dependents();
   if (ADAMAS_SEL_STOP == 9) return;  // diagnostics (timing only)
   for (int b = tid; b < kSelBins; b += kSelThreads) hist[b] = 0;
