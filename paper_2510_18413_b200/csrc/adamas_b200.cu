@@ -225,9 +225,9 @@ int ensure_unit_scratch(adamas_cache* c, size_t slots) {
 }
 
 // ----------------------------------------------------------------- fused launcher
-template <typename T, int G, int SW, int MODE, int CT = 0>
+template <typename T, int G, int SW, int MODE, int CT = 0, bool COLL = false>
 int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
-  auto kern = fused_decode_kernel<T, G, SW, MODE, CT>;
+  auto kern = fused_decode_kernel<T, G, SW, MODE, CT, COLL>;
   const int dev = current_device();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(prm.n_seqs * prm.n_kv * prm.qsplit * prm.P * C));
@@ -281,14 +281,18 @@ int launch_fused_t(FusedParams prm, int C, size_t smem, cudaStream_t s) {
 // multi-cluster units or candidates mode; the compaction form SW from the
 // rank length (spans cover it with 2 or 4 mask words, else 32-token groups).
 template <typename T, int G>
-int launch_fused_g(const FusedParams& prm, int C, size_t smem, cudaStream_t s, bool full, int sw) {
+int launch_fused_g(const FusedParams& prm, int C, size_t smem, cudaStream_t s, bool full, int sw, bool coll) {
   if (full) return sw == 2 ? launch_fused_t<T, G, 2, 1>(prm, C, smem, s) : launch_fused_t<T, G, 0, 1>(prm, C, smem, s);
   if (prm.cand) {  // lean candidates (sw 2, C 4, G <= 2: the one-hop shapes of sequence sharding)
-    if constexpr (G <= 2) return launch_fused_t<T, G, 2, 2, 4>(prm, C, smem, s);
+    if constexpr (G <= 2)
+      return coll ? launch_fused_t<T, G, 2, 2, 4, true>(prm, C, smem, s) : launch_fused_t<T, G, 2, 2, 4>(prm, C, smem, s);
     else return kFusedUnsupported;
   }
-  if (sw == 2) return C == 4 ? launch_fused_t<T, G, 2, 0, 4>(prm, C, smem, s) : launch_fused_t<T, G, 2, 0>(prm, C, smem, s);
-  if (sw == 4) return C == 1 ? launch_fused_t<T, G, 4, 0, 1>(prm, C, smem, s) : launch_fused_t<T, G, 4, 0>(prm, C, smem, s);
+  if (sw == 2) {
+    if (C == 4) return coll ? launch_fused_t<T, G, 2, 0, 4, true>(prm, C, smem, s) : launch_fused_t<T, G, 2, 0, 4>(prm, C, smem, s);
+    return launch_fused_t<T, G, 2, 0>(prm, C, smem, s);
+  }
+  if (sw == 4) return C == 1 ? launch_fused_t<T, G, 4, 0, 1, true>(prm, C, smem, s) : launch_fused_t<T, G, 4, 0, 0, true>(prm, C, smem, s);
   return launch_fused_t<T, G, 0, 0>(prm, C, smem, s);
 }
 
@@ -296,12 +300,13 @@ template <typename T>
 int launch_fused_dtype(const FusedParams& prm, int G, int C, size_t smem, cudaStream_t s) {
   const int64_t nt = kConsumers / G;
   const int sw = prm.chunk <= nt * 64 ? 2 : prm.chunk <= nt * 128 ? 4 : 0;
+  const bool coll = prm.chunk > nt * 16;  // spans of 32+ tokens per thread: collected-order masks
   // candidates mode has a lean instance for the common one-hop shape (sw 2, C 4; sequence sharding)
   const bool full = prm.P > 1 || C * G > 8 || (prm.cand != nullptr && !(sw == 2 && C == 4 && G <= 2));
   switch (G) {
-    case 1: return launch_fused_g<T, 1>(prm, C, smem, s, full, sw);
-    case 2: return launch_fused_g<T, 2>(prm, C, smem, s, full, sw);
-    case 4: return launch_fused_g<T, 4>(prm, C, smem, s, full, sw);
+    case 1: return launch_fused_g<T, 1>(prm, C, smem, s, full, sw, coll);
+    case 2: return launch_fused_g<T, 2>(prm, C, smem, s, full, sw, coll);
+    case 4: return launch_fused_g<T, 4>(prm, C, smem, s, full, sw, coll);
     case 8:  // test shapes only: one instance per mode, 32-token groups
       return full || prm.cand ? launch_fused_t<T, 8, 0, 1>(prm, C, smem, s) : launch_fused_t<T, 8, 0, 0>(prm, C, smem, s);
   }
