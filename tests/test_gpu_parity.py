@@ -227,6 +227,13 @@ def test_fused_compaction_span_sizes(gpu, oracle, tune, S, G):
     run_decode(gpu, oracle, S, 1, G, 128, True, seed=S + 13 * G, steps=2)
 
 
+@pytest.mark.parametrize("S,G", [(16000, 1), (40000, 1), (8000, 4)])
+def test_fused_compaction_span_sizes_fp32(gpu, oracle, tune, S, G):
+    """the same instances (collected-order masks for 32+-token spans) with fp32 K/V"""
+    tune(cluster=1)
+    run_decode(gpu, oracle, S, 1, G, 128, False, seed=S + 7 * G, steps=2)
+
+
 @pytest.mark.parametrize("cluster", ["1", "4"])
 def test_fused_decode_heavy_ties(gpu, oracle, tune, cluster):
     """keys drawn from 6 distinct vectors: whole bins of equal distances at T,
